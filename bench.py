@@ -1,0 +1,319 @@
+#!/usr/bin/env python
+"""Benchmark of the eventscope GMM hot path on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], "c2"): full-covariance GMM, K=8, D=16,
+N=2^26 SYN-v1 synthetic events (seed 42) resident in HBM, strong scaling
+over N GPUs (rank r owns rows [r N/G, (r+1) N/G)).  A step = one EM
+iteration (fused E+M pass, sufficient-statistics exchange, on-device M-step
+finalize, host convergence/collapse check).  Alongside, the scoring pass
+(detect: best-component density + flags + best_k + anomaly indices, Alg. 2)
+is timed the same way and reported under "score".
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Timing: W untimed steps, then K steps bracketed by barrier + device sync,
+CUDA events on the library's stream, max over ranks.  The event matrix
+(8.6 GB) is > L2 (126 MB), so no L2 flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_GLOBAL = 1 << 26
+D, K = 16, 8
+SEED = 42
+WORKLOAD = "gmm_em_full_K8_D16_N64M"
+METRIC = "EM iters/s (N=64M,D=16,K=8, full cov)"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler over the timed region."""
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if "Active" in r[2 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup(n_gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo")
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_baseline_sample(nthreads=None, iters=2, n_sample=1 << 19):
+    """Oracle (C++ FP64, OpenMP, all host cores) on a bounded sample of the
+    same workload: `iters` EM iterations on n_sample SYN-v1 rows; the per-event
+    rate is scaled to N=2^26 (time is linear in N)."""
+    from oracle import oracle
+    cores = nthreads or os.cpu_count()
+    model = oracle.syn_model(SEED, D, K)
+    X, _, _ = oracle.syn_rows(SEED, D, K, model, 0, n_sample, nthreads=cores)
+    pi0, mu0, cov0, reg = oracle.random_init(X, K, 7)
+    t0 = time.perf_counter()
+    oracle.fit_em(X, K, init_params=(pi0, mu0, cov0), tol=0.0, max_iter=iters, reg=reg, nthreads=cores)
+    dt = time.perf_counter() - t0
+    # fit_em with tol=0 runs `iters` E+M passes plus one final E pass
+    per_iter = dt / (iters + 0.5) * (N_GLOBAL / n_sample)
+    return {"value": 1.0 / per_iter, "unit": "iters/s", "cores": cores, "kind": "port",
+            "sample": f"{iters} EM iterations (+final E pass) of the CPU oracle on {n_sample} of the {N_GLOBAL} "
+                      f"SYN-v1 rows, {cores} OpenMP threads, scaled linearly to N={N_GLOBAL}"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_setup(args.gpus)
+    if rank != 0:
+        return
+    cores = os.cpu_count()
+    for _ in range(args.warmup):
+        pass
+    vals = []
+    for _ in range(max(1, args.steps)):
+        vals.append(cpu_baseline_sample(cores, iters=1, n_sample=1 << 18)["value"])
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / v, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (SYN-v1, seed 42)",
+            "config": {"workload": WORKLOAD, "N": N_GLOBAL, "D": D, "K": K, "covariance": "full"},
+            "cpu_baseline": {"value": v, "unit": "iters/s", "cores": cores, "kind": "port",
+                             "sample": "per step: 1 EM iteration (+final E pass) of the CPU oracle on 2^18 SYN-v1 "
+                                       "rows, all host threads, scaled linearly to N=2^26"},
+            "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2506_02007_b200 as es
+
+    rank, world, local = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        obj = [es.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = es.Context(local, rank, world, nccl_id=obj[0])
+    else:
+        ctx = es.Context(local)
+    n_global = args.n or N_GLOBAL
+    ds = es.Dataset.generate(SEED, n_global, D, K, ctx=ctx)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    lib = ctx._lib
+    import ctypes as C
+
+    def ktime(which):
+        ms, n = C.c_double(), C.c_int64()
+        lib.es_ctx_kernel_time(ctx.handle, which, C.byref(ms), C.byref(n))
+        return ms.value, n.value
+
+    # ------------------------------------------------------------ EM steps
+    total = args.warmup + args.steps
+    em = es.EM(ds, K, init="random", tol=0.0, max_iter=total + 1, seed=7)
+    for _ in range(args.warmup):
+        em.step(1)
+    barrier(world)
+    torch.cuda.synchronize()
+    lib.es_ctx_set_timing(ctx.handle, 1)
+    l0 = ctx.launch_count
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            em.step(1)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    em_launches = ctx.launch_count - l0
+    em_ms = e0.elapsed_time(e1)
+    kern_ms, kern_n = ktime(0)
+    lib.es_ctx_set_timing(ctx.handle, 0)
+    barrier(world)
+    em_ms_max = max_over_ranks(em_ms, world)
+    model = em.finish()
+    em.close()
+
+    # ----------------------------------------------------------- scoring
+    n_loc = ds.n_local
+    flags = torch.empty(n_loc, dtype=torch.uint8, device="cuda")
+    bk = torch.empty(n_loc, dtype=torch.int32, device="cuda")
+    bl = torch.empty(n_loc, dtype=torch.float64, device="cuda")
+    d, ld = es.calibrate_threshold(model, ds, 0.01, n_train=n_global // 2, return_log=True)
+    for _ in range(max(args.warmup, 1)):
+        es.detect(model, ds, log_delta=ld, flags=flags, best_k=bk, best_logdens=bl, indices=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    lib.es_ctx_set_timing(ctx.handle, 1)
+    l1 = ctx.launch_count
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    nflag = 0
+    for _ in range(args.steps):
+        r = es.detect(model, ds, log_delta=ld, flags=flags, best_k=bk, best_logdens=bl, indices=True)
+        nflag = r.n_flagged
+    s1.record(stream)
+    torch.cuda.synchronize()
+    sc_launches = ctx.launch_count - l1
+    sc_ms = max_over_ranks(s0.elapsed_time(s1), world)
+    sk_ms, sk_n = ktime(1)
+    lib.es_ctx_set_timing(ctx.handle, 0)
+
+    # ------------------------------------------- e2e through the public API
+    # host (pinned) event matrix -> es_dataset_create (H2D) -> EM iterations
+    # -> parameters back to the host, all inside the timed region.
+    e2e = None
+    if not args.no_e2e:
+        hostX = torch.empty((ds.n_local, D), dtype=torch.float64, pin_memory=True)
+        ds.read_rows(out=hostX)
+        e2e_iters = max(args.steps, 1)
+        barrier(world)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ds2 = es.Dataset.from_array(hostX.numpy(), ctx=ctx)
+        em2 = es.EM(ds2, K, init="random", tol=0.0, max_iter=e2e_iters, seed=7)
+        em2.step(e2e_iters)
+        m2 = em2.finish()
+        torch.cuda.synchronize()
+        e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+        em2.close()
+        ds2.close()
+        h2d = hostX.numel() * 8 * world
+        d2h = (K + K * D + K * D * D) * 8 * world
+        e2e = {"value": e2e_iters / e2e_s, "unit": "iters/s", "h2d_bytes_per_step": h2d / e2e_iters,
+               "d2h_bytes_per_step": d2h / e2e_iters,
+               "note": f"per call: H2D of the {n_global}x{D} f64 matrix + data stats + Random init + {e2e_iters} "
+                       f"EM iterations + final logL + params D2H; steps = EM iterations",
+               "final_log_likelihood": m2.fit_report.final_log_likelihood}
+        del hostX
+
+    if rank != 0:
+        return
+    hbm, src = peaks()
+    it_s = args.steps / (em_ms_max / 1e3)
+    bytes_iter = n_global * D * 8
+    em_kern_avg = kern_ms / max(kern_n, 1)
+    ach = (bytes_iter / world) / (em_kern_avg / 1e3) / 1e9
+    sc_evs = n_global * args.steps / (sc_ms / 1e3)
+    sc_kern_avg = sk_ms / max(sk_n, 1)
+    sc_bytes = (n_global / world) * (D * 8 + 13)
+    sc_ach = sc_bytes / (sc_kern_avg / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": it_s, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": em_ms_max / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (SYN-v1 seed 42, device generated)",
+        "config": {"workload": WORKLOAD, "N": n_global, "D": D, "K": K, "covariance": "full", "init": "random seed 7",
+                   "l2": "inputs (8.6 GB) larger than L2; no flush", "parallelism": f"rows sharded over {world} GPU(s)"},
+        "roofline": {"bound": "hbm", "kernel": "k_em_team<16,2>", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                     "frac": ach / hbm, "peak_source": src, "traffic": None,
+                     "algorithmic_bytes_per_launch": bytes_iter / world, "avg_launch_ms": em_kern_avg,
+                     "kernel_share_of_step": kern_ms / em_ms if em_ms else None},
+        "score": {"events_per_s": sc_evs, "ms_per_pass": sc_ms / args.steps, "n_flagged": nflag,
+                  "roofline": {"bound": "hbm", "kernel": "k_score_team<16>", "achieved": sc_ach, "peak": hbm,
+                               "unit": "GB/s", "frac": sc_ach / hbm,
+                               "algorithmic_bytes_per_launch": sc_bytes, "avg_launch_ms": sc_kern_avg}},
+        "gpu_launches": em_launches,
+        "gpu_launches_score": sc_launches,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_sample()
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=0, help="override N (debug only)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

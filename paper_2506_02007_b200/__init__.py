@@ -1,0 +1,473 @@
+"""eventscope-b200: B200-native GMM EM fitting, scoring and anomaly detection.
+
+Python view of the C-ABI in include/eventscope_b200.h (the product is the
+CUDA library paper_2506_02007_b200/lib/libeventscope_b200.so; this module is
+a thin ctypes binding used by tests, bench.py and Python callers).  Names,
+argument meaning and errors mirror the reference's operator interface
+(SPEC.md gmm-core / anomaly-detect ops, errors.hpp ErrorKind + stable names):
+
+    fit_em
+    component_log_density
+    mixture_density
+    responsibilities
+    select_k_bic
+    detect
+    calibrate_threshold
+    score_samples / predict (batched log-density / argmax posterior)
+
+There is no CPU fallback: if the extension is missing or no CUDA device is
+present, calls raise EventscopeError(kind="Io", name="CudaError"/"NotBuilt").
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from ._build import LIB as _LIB_PATH
+
+__all__ = [
+    "EventscopeError", "Context", "Dataset", "GmmModel", "FitReport", "DetectionReport",
+    "fit_em", "component_log_density", "mixture_density", "responsibilities", "select_k_bic",
+    "score_samples", "predict", "detect", "calibrate_threshold", "default_context", "load_library",
+    "ES_INIT_RANDOM", "ES_INIT_KMEANSPP", "ES_INIT_GIVEN",
+]
+
+ES_INIT_RANDOM, ES_INIT_KMEANSPP, ES_INIT_GIVEN = 0, 1, 2
+_KIND = {1: "Data", 2: "Numeric", 3: "Io", 4: "Io"}
+
+
+class EventscopeError(RuntimeError):
+    """Mirror of eventscope::Error (errors.hpp:21-37): kind + stable name."""
+
+    def __init__(self, kind: str, name: str, message: str):
+        super().__init__(f"{name}: {message}")
+        self.kind = kind
+        self.name = name
+
+
+class _Params(C.Structure):
+    _fields_ = [("K", C.c_int32), ("D", C.c_int32), ("weights", C.c_void_p), ("means", C.c_void_p),
+                ("covariances", C.c_void_p)]
+
+
+class _FitOpts(C.Structure):
+    _fields_ = [("init", C.c_int32), ("tol", C.c_double), ("max_iter", C.c_int32), ("reg", C.c_double),
+                ("seed", C.c_uint64)]
+
+
+class _FitReport(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("final_log_likelihood", C.c_double), ("converged", C.c_int32),
+                ("seed", C.c_uint64), ("n_per_iter", C.c_int32), ("collapses", C.c_int32),
+                ("reg_used", C.c_double)]
+
+
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_int)
+
+
+class _Exchange(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("allgather", ALLGATHER_FN), ("allreduce", ALLREDUCE_FN)]
+
+
+_lib = None
+
+
+def load_library() -> C.CDLL:
+    """Load the in-tree CUDA library (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise EventscopeError("Io", "NotBuilt",
+                                  f"{_LIB_PATH} missing; run __graft_entry__.build() (no CPU fallback exists)")
+        lib = C.CDLL(_LIB_PATH)
+        lib.es_last_error_name.restype = C.c_char_p
+        lib.es_last_error_message.restype = C.c_char_p
+        lib.es_version.restype = C.c_char_p
+        _lib = lib
+    return _lib
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        lib = load_library()
+        raise EventscopeError(_KIND.get(status, "Io"), lib.es_last_error_name().decode(),
+                              lib.es_last_error_message().decode())
+
+
+def _ptr(a) -> Optional[int]:
+    """Address of a numpy array or torch tensor (host or device); None passes NULL."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    return a.ctypes.data
+
+
+@dataclass
+class FitReport:
+    iterations: int = 0
+    final_log_likelihood: float = 0.0
+    per_iteration_log_likelihoods: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    converged: bool = False
+    seed: int = 0
+    collapses: int = 0
+    reg: float = 0.0
+
+
+@dataclass
+class GmmModel:
+    """weights (K), means (K,d), covariances (K,d,d)."""
+    weights: np.ndarray
+    means: np.ndarray
+    covariances: np.ndarray
+    fit_report: FitReport = field(default_factory=FitReport)
+
+    @property
+    def K(self) -> int:
+        return int(self.weights.shape[0])
+
+    @property
+    def d(self) -> int:
+        return int(self.means.shape[1])
+
+    def _c(self):
+        w = np.ascontiguousarray(self.weights, np.float64)
+        m = np.ascontiguousarray(self.means, np.float64)
+        c = np.ascontiguousarray(self.covariances, np.float64)
+        if m.ndim != 2 or m.shape[0] != w.shape[0] or c.shape != (w.shape[0], m.shape[1], m.shape[1]):
+            raise EventscopeError("Data", "InvalidModel", "weights/means/covariances shapes disagree")
+        p = _Params(w.shape[0], m.shape[1], w.ctypes.data, m.ctypes.data, c.ctypes.data)
+        return p, (w, m, c)
+
+
+@dataclass
+class DetectionReport:
+    """SPEC.md:351-354."""
+    flags: np.ndarray
+    anomaly_indices: np.ndarray
+    best_component: np.ndarray
+    log_density: np.ndarray
+    model: GmmModel
+    delta: float
+    log_delta: float
+    n_flagged: int = 0
+
+
+class Context:
+    """One GPU (one process per GPU).  world>1 uses NCCL (nccl_id) or host
+    exchange callbacks (exchange=(allgather_fn, allreduce_fn))."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
+                 exchange=None):
+        lib = load_library()
+        self._lib = lib
+        h = C.c_void_p()
+        self._keep = None
+        if world > 1 and exchange is not None:
+            ag, ar = exchange
+            ex = _Exchange(None, ALLGATHER_FN(ag), ALLREDUCE_FN(ar))
+            self._keep = ex
+            _check(lib.es_ctx_create_exchange(device, rank, world, C.byref(ex), C.byref(h)))
+        elif world > 1:
+            idb = (C.c_ubyte * 128).from_buffer_copy(nccl_id)
+            _check(lib.es_ctx_create_nccl(device, rank, world, idb, C.byref(h)))
+        else:
+            _check(lib.es_ctx_create(device, C.byref(h)))
+        self.handle = h
+        self.device, self.rank, self.world = device, rank, world
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_ubyte * 128)()
+        _check(load_library().es_nccl_unique_id(buf))
+        return bytes(buf)
+
+    @property
+    def stream(self) -> int:
+        s = C.c_void_p()
+        _check(self._lib.es_ctx_stream(self.handle, C.byref(s)))
+        return s.value or 0
+
+    @property
+    def launch_count(self) -> int:
+        n = C.c_int64()
+        _check(self._lib.es_ctx_launch_count(self.handle, C.byref(n)))
+        return n.value
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self._lib.es_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(int(os.environ.get("ES_DEVICE", "0")))
+    return _default_ctx
+
+
+class Dataset:
+    """This rank's event rows, resident in HBM (feature-planar FP64)."""
+
+    def __init__(self, ctx: Context, handle: C.c_void_p):
+        self.ctx = ctx
+        self.handle = handle
+        nl, ng, off, d = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int32()
+        _check(ctx._lib.es_dataset_info(handle, C.byref(nl), C.byref(ng), C.byref(off), C.byref(d)))
+        self.n_local, self.n_global, self.row_offset, self.D = nl.value, ng.value, off.value, d.value
+
+    @classmethod
+    def from_array(cls, X, ctx: Optional[Context] = None) -> "Dataset":
+        """X: numpy (N,D) float64 (any strides) or a CUDA torch tensor (row- or column-major)."""
+        ctx = ctx or default_context()
+        if hasattr(X, "data_ptr"):
+            n, d = X.shape
+            rs, cs = X.stride()
+            ptr = X.data_ptr()
+        else:
+            X = np.asarray(X, np.float64)
+            if X.ndim == 1:
+                X = X[:, None]
+            n, d = X.shape
+            rs, cs = X.strides[0] // 8, X.strides[1] // 8
+            if X.strides[0] % 8 or X.strides[1] % 8:
+                X = np.ascontiguousarray(X)
+                rs, cs = d, 1
+            ptr = X.ctypes.data
+        h = C.c_void_p()
+        _check(ctx._lib.es_dataset_create(ctx.handle, C.c_void_p(ptr), C.c_int64(n), C.c_int32(d),
+                                          C.c_int64(rs), C.c_int64(cs), C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def generate(cls, seed: int, n_global: int, D: int, K_true: int, ctx: Optional[Context] = None) -> "Dataset":
+        """SYN-v1 synthetic events generated on the device (this rank's shard)."""
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        _check(ctx._lib.es_dataset_generate(ctx.handle, C.c_uint64(seed), C.c_int64(n_global), C.c_int32(D),
+                                            C.c_int32(K_true), C.byref(h)))
+        return cls(ctx, h)
+
+    def read_rows(self, row0: int = 0, n: Optional[int] = None, out=None):
+        """Rows [row0, row0+n) row-major into `out` (numpy / pinned or CUDA tensor) or a new array."""
+        n = self.n_local - row0 if n is None else n
+        if out is None:
+            out = np.empty((n, self.D))
+        _check(self.ctx._lib.es_dataset_read_rows(self.handle, C.c_int64(row0), C.c_int64(n),
+                                                  C.c_void_p(_ptr(out))))
+        return out
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self.ctx._lib.es_dataset_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _as_dataset(X, ctx: Optional[Context]) -> Dataset:
+    return X if isinstance(X, Dataset) else Dataset.from_array(X, ctx)
+
+
+def _opts(init, tol, max_iter, reg, seed) -> _FitOpts:
+    code = {"random": ES_INIT_RANDOM, "kmeans++": ES_INIT_KMEANSPP, "kmeanspp": ES_INIT_KMEANSPP,
+            "given": ES_INIT_GIVEN}[init] if isinstance(init, str) else int(init)
+    env = os.environ.get("EACGM_SEED")
+    if env is not None:
+        seed = int(env)
+    return _FitOpts(code, float(tol), int(max_iter), -1.0 if reg is None else float(reg), int(seed))
+
+
+class EM:
+    """Stepwise EM engine (es_gmm_em_begin/step/end): same semantics as fit_em."""
+
+    def __init__(self, X, K: int, init="kmeans++", tol=1e-6, max_iter=200, reg=None, seed=0,
+                 init_params: Optional[GmmModel] = None, ctx: Optional[Context] = None):
+        self.ds = _as_dataset(X, ctx)
+        self.ctx = self.ds.ctx
+        self.K = K
+        o = _opts("given" if init_params is not None else init, tol, max_iter, reg, seed)
+        self.max_iter = o.max_iter
+        keep = None
+        pp = None
+        if init_params is not None:
+            p, keep = init_params._c()
+            pp = C.byref(p)
+        h = C.c_void_p()
+        _check(self.ctx._lib.es_gmm_em_begin(self.ctx.handle, self.ds.handle, C.c_int32(K), C.byref(o), pp,
+                                             C.byref(h)))
+        del keep
+        self.handle = h
+        self.done = False
+
+    def step(self, n: int = 1) -> bool:
+        d = C.c_int32()
+        _check(self.ctx._lib.es_gmm_em_step(self.handle, C.c_int32(n), C.byref(d)))
+        self.done = bool(d.value)
+        return self.done
+
+    def finish(self) -> GmmModel:
+        K, D = self.K, self.ds.D
+        w, m, c = np.empty(K), np.empty((K, D)), np.empty((K, D, D))
+        out = _Params(K, D, w.ctypes.data, m.ctypes.data, c.ctypes.data)
+        rep = _FitReport()
+        per = np.empty(self.max_iter + 1)
+        _check(self.ctx._lib.es_gmm_em_end(self.handle, C.byref(out), C.byref(rep), C.c_void_p(per.ctypes.data)))
+        fr = FitReport(rep.iterations, rep.final_log_likelihood, per[:rep.n_per_iter].copy(), bool(rep.converged),
+                       rep.seed, rep.collapses, rep.reg_used)
+        return GmmModel(w, m, c, fr)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self.ctx._lib.es_gmm_em_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def fit_em(X, K: int, init="kmeans++", tol: float = 1e-6, max_iter: int = 200, reg: Optional[float] = None,
+           seed: int = 0, init_params: Optional[GmmModel] = None, ctx: Optional[Context] = None) -> GmmModel:
+    """EM fit.  Defaults per SPEC.md:319-321."""
+    em = EM(X, K, init, tol, max_iter, reg, seed, init_params, ctx)
+    try:
+        em.step(max(max_iter, 0))
+        return em.finish()
+    finally:
+        em.close()
+
+
+def score(model: GmmModel, X, ctx: Optional[Context] = None, ll=None, predict=None, best_k=None,
+          best_logdens=None) -> float:
+    """Batched scoring into caller buffers (numpy or CUDA tensors); returns global sum of ll."""
+    ds = _as_dataset(X, ctx)
+    p, keep = model._c()
+    tot = C.c_double()
+    _check(ds.ctx._lib.es_gmm_score(ds.ctx.handle, ds.handle, C.byref(p), C.c_void_p(_ptr(ll)),
+                                    C.c_void_p(_ptr(predict)), C.c_void_p(_ptr(best_k)),
+                                    C.c_void_p(_ptr(best_logdens)), C.byref(tot)))
+    del keep
+    return tot.value
+
+
+def score_samples(model: GmmModel, X, ctx: Optional[Context] = None) -> np.ndarray:
+    ds = _as_dataset(X, ctx)
+    ll = np.empty(ds.n_local)
+    score(model, ds, ll=ll)
+    return ll
+
+
+def predict(model: GmmModel, X, ctx: Optional[Context] = None) -> np.ndarray:
+    ds = _as_dataset(X, ctx)
+    pr = np.empty(ds.n_local, np.int32)
+    score(model, ds, predict=pr)
+    return pr
+
+
+def responsibilities(model: GmmModel, X, ctx: Optional[Context] = None) -> np.ndarray:
+    ds = _as_dataset(X, ctx)
+    p, keep = model._c()
+    g = np.empty((ds.n_local, model.K))
+    _check(ds.ctx._lib.es_gmm_responsibilities(ds.ctx.handle, ds.handle, C.byref(p), C.c_void_p(g.ctypes.data)))
+    del keep
+    return g
+
+
+def component_log_density(model: GmmModel, x, k: int, ctx: Optional[Context] = None) -> float:
+    ctx = ctx or default_context()
+    x = np.ascontiguousarray(x, np.float64).reshape(-1)
+    if x.shape[0] != model.d:
+        raise EventscopeError("Data", "DimensionMismatch", "x has the wrong dimension")
+    p, keep = model._c()
+    out = C.c_double()
+    _check(ctx._lib.es_gmm_component_log_density(ctx.handle, C.byref(p), C.c_void_p(x.ctypes.data),
+                                                 C.c_int32(k), C.byref(out)))
+    del keep
+    return out.value
+
+
+def mixture_density(model: GmmModel, x, ctx: Optional[Context] = None) -> float:
+    ctx = ctx or default_context()
+    x = np.ascontiguousarray(x, np.float64).reshape(-1)
+    if x.shape[0] != model.d:
+        raise EventscopeError("Data", "DimensionMismatch", "x has the wrong dimension")
+    p, keep = model._c()
+    out = C.c_double()
+    _check(ctx._lib.es_gmm_mixture_log_density(ctx.handle, C.byref(p), C.c_void_p(x.ctypes.data), C.byref(out)))
+    del keep
+    return float(np.exp(out.value))
+
+
+def detect(model: GmmModel, X, delta: Optional[float] = None, mode: str = "component",
+           log_delta: Optional[float] = None, ctx: Optional[Context] = None, flags=None, best_k=None,
+           best_logdens=None, indices: bool = True) -> DetectionReport:
+    """Def. 1 / Alg. 2: flag iff log p < log delta (strict)."""
+    if log_delta is None:
+        if delta is None or not delta > 0:
+            raise EventscopeError("Data", "RangeViolation", "delta must be > 0")
+        log_delta = float(np.log(delta)) if np.isfinite(delta) else float("inf")
+    ds = _as_dataset(X, ctx)
+    p, keep = model._c()
+    n = ds.n_local
+    fl = np.empty(n, np.uint8) if flags is None else flags
+    bk = np.empty(n, np.int32) if best_k is None else best_k
+    bl = np.empty(n) if best_logdens is None else best_logdens
+    idx = np.empty(max(n, 1), np.int64) if indices else None
+    nloc, ng = C.c_int64(), C.c_int64()
+    m = {"component": 0, "mixture": 1}[mode]
+    _check(ds.ctx._lib.es_gmm_detect(ds.ctx.handle, ds.handle, C.byref(p), C.c_double(log_delta), C.c_int32(m),
+                                     C.c_void_p(_ptr(fl)), C.c_void_p(_ptr(bk)), C.c_void_p(_ptr(bl)),
+                                     C.c_void_p(_ptr(idx)), C.byref(nloc), C.byref(ng)))
+    del keep
+    A = idx[:nloc.value].copy() if indices else np.zeros(0, np.int64)
+    d = float(np.exp(log_delta)) if delta is None else float(delta)
+    return DetectionReport(fl, A, bk, bl, model, d, float(log_delta), ng.value)
+
+
+def calibrate_threshold(model: GmmModel, X_train, q: float, mode: str = "component", n_train: Optional[int] = None,
+                        ctx: Optional[Context] = None, return_log: bool = False):
+    """delta = q-quantile of best-component densities over the train rows."""
+    ds = _as_dataset(X_train, ctx)
+    nt = ds.n_global if n_train is None else n_train
+    p, keep = model._c()
+    d, ld = C.c_double(), C.c_double()
+    m = {"component": 0, "mixture": 1}[mode]
+    _check(ds.ctx._lib.es_gmm_calibrate(ds.ctx.handle, ds.handle, C.byref(p), C.c_int64(nt), C.c_double(q),
+                                        C.c_int32(m), C.byref(d), C.byref(ld)))
+    del keep
+    return (d.value, ld.value) if return_log else d.value
+
+
+def select_k_bic(X, k_range: Sequence[int], init="kmeans++", tol=1e-6, max_iter=200, reg=None, seed=0,
+                 ctx: Optional[Context] = None):
+    """(best_K, bic_values); failed K -> NaN."""
+    ds = _as_dataset(X, ctx)
+    kr = np.ascontiguousarray(list(k_range), np.int32)
+    bic = np.empty(len(kr))
+    best = C.c_int32()
+    o = _opts(init, tol, max_iter, reg, seed)
+    _check(ds.ctx._lib.es_gmm_select_k_bic(ds.ctx.handle, ds.handle, C.c_void_p(kr.ctypes.data),
+                                           C.c_int32(len(kr)), C.byref(o), C.byref(best),
+                                           C.c_void_p(bic.ctypes.data)))
+    return best.value, bic

@@ -1,0 +1,78 @@
+// es_kernels.h — launchers for the sm_100a kernels (es_kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "es_layout.h"
+
+namespace es {
+
+constexpr int kBlock = 256;
+
+// Per-event outputs of a scoring pass; any pointer may be null.
+struct ScoreOut {
+    double* ll = nullptr;          // log p(x_i)
+    int32_t* predict = nullptr;    // argmax_k log pi_k + log N_ik
+    int32_t* best_k = nullptr;     // argmax_k log N_ik
+    double* best_ld = nullptr;     // log N_{i,best_k}
+    uint8_t* flags = nullptr;      // (mode value) < log_delta
+    double* gamma = nullptr;       // n x K responsibilities
+    double* lnk = nullptr;         // n x K component log densities
+    double log_delta = 0.0;
+    int mode = 0;                  // 0 component, 1 mixture
+};
+
+struct LaunchStats {
+    int64_t launches = 0;
+};
+
+// Which EM pass implementation a (D, K) shape uses.
+enum class EmPath { Team4, Team8, Team16, Generic };
+EmPath em_path(int D, int K);
+// Number of CTA partial blocks the EM pass writes for this shape.
+int em_grid(int D, int K, int num_sms);
+int score_grid(int D, int K, int num_sms);
+
+// EM E+M pass: writes grid partial stat blocks (stat_total(D,K) doubles each)
+// into `partial`; returns the grid size through *nblk.  `whitened` reports
+// the coordinate system of the statistics.
+void launch_em_pass(const double* X, int64_t n, int64_t ld, int D, int K, const double* model, double* partial,
+                    int num_sms, int* nblk, bool* whitened, cudaStream_t s, LaunchStats& ls);
+// Unit-weight statistics about `center` (K = 1): data covariance pass.
+void launch_unit_stats(const double* X, int64_t n, int64_t ld, int D, const double* center, double* partial,
+                       int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
+// Fixed-order sum of nblk partial blocks of length len -> out.
+void launch_reduce_blocks(const double* partial, int nblk, int len, double* out, cudaStream_t s, LaunchStats& ls);
+// Column sum/min/max/non-finite count: out[4*D] = sum | min | max | nonfinite.
+void launch_col_stats(const double* X, int64_t n, int64_t ld, int D, double* scratch, double* out, int num_sms,
+                      cudaStream_t s, LaunchStats& ls);
+// M-step finalize from G rank blocks of statistics (summed in rank order),
+// updating the model in place and writing IterStatus (+ logL record[t]).
+void launch_finalize(const double* stats, int G, int D, int K, int64_t n_global, double reg, bool whitened,
+                     double* model, IterStatus* st, double* record, int t, cudaStream_t s, LaunchStats& ls);
+// Derive L, W, lognorm, logpi from pi, mu, cov in `model` (all components).
+void launch_derive(double* model, int D, int K, IterStatus* st, cudaStream_t s, LaunchStats& ls);
+// Scoring pass; `blocksum` receives per-CTA [ll_sum, flag_count] pairs.
+void launch_score(const double* X, int64_t n, int64_t ld, int D, int K, const double* model, const ScoreOut& o,
+                  double* blocksum, int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
+// Order-preserving radix select helpers on FP64 keys.
+void launch_hist8(const double* keys, int64_t n, int shift, uint64_t prefix_mask, uint64_t prefix_val,
+                  unsigned long long* hist, int num_sms, cudaStream_t s, LaunchStats& ls);
+// Anomaly-index compaction (order preserving).
+void launch_compact(const uint8_t* flags, int64_t n, int64_t index_base, int64_t* counts_scratch,
+                    int64_t* out_idx, int64_t* out_count, cudaStream_t s, LaunchStats& ls);
+// Row-major staging -> planar transpose for rows [row0, row0+n).
+void launch_rows_to_planar(const double* rows, int64_t n, int D, double* X, int64_t ld, int64_t row0,
+                           cudaStream_t s, LaunchStats& ls);
+// Planar -> row-major for rows [row0, row0+n).
+void launch_planar_to_rows(const double* X, int64_t ld, int D, int64_t row0, int64_t n, double* rows,
+                           cudaStream_t s, LaunchStats& ls);
+// k-means++ distance update: d2[i] = min(d2[i], ||x_i - c||^2) (first: assign),
+// parts[chunk] = fixed-order sum of d2 over 4096-row chunks.
+void launch_kpp_update(const double* X, int64_t n, int64_t ld, int D, const double* center, double* d2,
+                       double* parts, bool first, cudaStream_t s, LaunchStats& ls);
+// SYN-v1 rows [grow0, grow0+n) written into planar X (local row = global - grow0).
+void launch_synth(double* X, int64_t ld, int64_t n, int64_t grow0, int D, int K, const double* syn_model,
+                  uint64_t seed, cudaStream_t s, LaunchStats& ls);
+
+}  // namespace es

@@ -1,0 +1,1209 @@
+// es_runtime.cu — host runtime behind the C-ABI (include/eventscope_b200.h).
+//
+// One context per GPU (one process per GPU under torchrun / MPI).  A dataset
+// is the rank's contiguous block of event rows, resident in HBM in the
+// feature-planar layout of es_layout.h.  The EM loop per iteration is
+//   em_pass (fused E + M statistics, per-CTA partials)
+//   -> fixed-order block reduce -> rank exchange (NCCL all-gather over NVLink)
+//   -> finalize (rank-ordered sum, M-step, Cholesky, W = L^-1, logL record)
+//   -> 40-byte IterStatus read by the host (convergence / collapse decisions).
+// Control semantics follow SPEC.md:291-299,319-326,335 exactly as the CPU
+// oracle restates them (oracle/es_oracle.cpp), including the host PRNG
+// (SplitMix64) so that Random / k-means++ init and collapse reseeds draw the
+// same rows.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: NCCL is resolved at run time (see Nccl below)
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/eventscope_b200.h"
+#include "es_kernels.h"
+
+using namespace es;
+
+namespace {
+
+thread_local std::string g_name;
+thread_local std::string g_msg;
+
+struct Fail {
+    int code;
+    std::string name;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& name, const std::string& msg) { throw Fail{code, name, msg}; }
+
+void cu_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(ES_ERR_RUNTIME, "CudaError", std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CU(x) cu_check((x), #x)
+
+// NCCL is bound lazily with dlopen instead of at link time: a process that
+// already loaded a libnccl.so.2 (e.g. PyTorch's bundled 2.28) keeps using it,
+// and a process that never builds a multi-GPU context never loads NCCL.
+struct Nccl {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const Nccl& nccl();
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        fail(ES_ERR_RUNTIME, "NcclError", std::string(what) + ": " + nccl().GetErrorString(r));
+}
+#define NC(x) nccl_check((x), #x)
+
+const Nccl& nccl() {
+    static Nccl n;
+    static bool loaded = false;
+    if (loaded) return n;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) fail(ES_ERR_RUNTIME, "NcclError", std::string("cannot load libnccl.so.2: ") + dlerror());
+    auto sym = [&](const char* name) {
+        void* p = dlsym(h, name);
+        if (!p) fail(ES_ERR_RUNTIME, "NcclError", std::string("missing NCCL symbol ") + name);
+        return p;
+    };
+    n.GetUniqueId = reinterpret_cast<decltype(n.GetUniqueId)>(sym("ncclGetUniqueId"));
+    n.CommInitRank = reinterpret_cast<decltype(n.CommInitRank)>(sym("ncclCommInitRank"));
+    n.CommDestroy = reinterpret_cast<decltype(n.CommDestroy)>(sym("ncclCommDestroy"));
+    n.AllGather = reinterpret_cast<decltype(n.AllGather)>(sym("ncclAllGather"));
+    n.AllReduce = reinterpret_cast<decltype(n.AllReduce)>(sym("ncclAllReduce"));
+    n.GetErrorString = reinterpret_cast<decltype(n.GetErrorString)>(sym("ncclGetErrorString"));
+    loaded = true;
+    return n;
+}
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return ES_OK;
+    } catch (const Fail& e) {
+        g_name = e.name;
+        g_msg = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_name = "OutOfMemory";
+        g_msg = "host allocation failed";
+        return ES_ERR_RUNTIME;
+    } catch (const std::exception& e) {
+        g_name = "RuntimeError";
+        g_msg = e.what();
+        return ES_ERR_RUNTIME;
+    }
+}
+
+// SplitMix64 — the documented host PRNG ("named, portable 64-bit
+// generator"); identical draws to the oracle's.
+struct SplitMix64 {
+    uint64_t s;
+    explicit SplitMix64(uint64_t seed) : s(seed) {}
+    uint64_t next() {
+        uint64_t z = (s += 0x9E3779B97F4A7C15ull);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        return z ^ (z >> 31);
+    }
+    uint64_t below(uint64_t n) { return (uint64_t)(((unsigned __int128)next() * n) >> 64); }
+    double uniform() { return (double)(next() >> 11) * 0x1.0p-53; }
+};
+
+// Growable device buffer.
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* get(size_t bytes) {
+        if (bytes > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cap = 0;
+            CU(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+            cap = std::max<size_t>(bytes, 256);
+        }
+        return p;
+    }
+    template <class T>
+    T* as(size_t count) {
+        return static_cast<T*>(get(count * sizeof(T)));
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+// ================================================================ structs
+struct es_ctx {
+    int device = 0, rank = 0, world = 1;
+    int mode = 0;  // 0 single, 1 nccl, 2 host exchange
+    ncclComm_t comm = nullptr;
+    es_exchange ex{};
+    cudaStream_t stream = nullptr;
+    int num_sms = 148;
+    LaunchStats ls;
+    DevBuf partial, stats_local, stats_all, model, model_backup, status, scratch, scratch2, scratch3, out_scratch,
+        hist, xbuf, o1, o2, o3, o4, o5;
+    IterStatus* h_status = nullptr;  // pinned
+    std::vector<double> hbuf;
+    // optional CUDA-event timing of the hot kernels (bench.py roofline)
+    bool timing = false;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    double em_ms = 0.0, score_ms = 0.0;
+    int64_t em_launches = 0, score_launches = 0;
+    void t_begin() {
+        if (timing) CU(cudaEventRecord(ev0, stream));
+    }
+    void t_end(double& acc, int64_t& cnt) {
+        if (!timing) return;
+        CU(cudaEventRecord(ev1, stream));
+        CU(cudaEventSynchronize(ev1));
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, ev0, ev1));
+        acc += ms;
+        ++cnt;
+    }
+
+    void sync() { CU(cudaStreamSynchronize(stream)); }
+    void check_launch() { CU(cudaGetLastError()); }
+
+    // All-gather count doubles per rank (device in/out).
+    void allgather(const double* d_send, double* d_recv, size_t count) {
+        if (world == 1) {
+            if (d_send != d_recv) CU(cudaMemcpyAsync(d_recv, d_send, count * 8, cudaMemcpyDeviceToDevice, stream));
+        } else if (mode == 1) {
+            NC(nccl().AllGather(d_send, d_recv, count, ncclFloat64, comm, stream));
+        } else {
+            std::vector<double> s(count), r(count * world);
+            CU(cudaMemcpyAsync(s.data(), d_send, count * 8, cudaMemcpyDeviceToHost, stream));
+            sync();
+            if (ex.allgather(ex.user, s.data(), r.data(), count * 8) != 0)
+                fail(ES_ERR_RUNTIME, "ExchangeError", "allgather callback failed");
+            CU(cudaMemcpyAsync(d_recv, r.data(), count * world * 8, cudaMemcpyHostToDevice, stream));
+            sync();
+        }
+    }
+    // In-place all-reduce on HOST memory (small control values).
+    void allreduce_host(void* buf, size_t count, int dtype, int op) {
+        if (world == 1) return;
+        if (mode == 2) {
+            if (ex.allreduce(ex.user, buf, count, dtype, op) != 0)
+                fail(ES_ERR_RUNTIME, "ExchangeError", "allreduce callback failed");
+            return;
+        }
+        const size_t bytes = count * 8;
+        void* d = xbuf.get(bytes);
+        CU(cudaMemcpyAsync(d, buf, bytes, cudaMemcpyHostToDevice, stream));
+        const ncclDataType_t t = dtype == 0 ? ncclFloat64 : ncclInt64;
+        const ncclRedOp_t o = op == 0 ? ncclSum : op == 1 ? ncclMin : ncclMax;
+        NC(nccl().AllReduce(d, d, count, t, o, comm, stream));
+        CU(cudaMemcpyAsync(buf, d, bytes, cudaMemcpyDeviceToHost, stream));
+        sync();
+    }
+    // Rank-ordered all-gather of host values.
+    std::vector<double> allgather_host(const double* v, size_t count) {
+        std::vector<double> r(count * world);
+        if (world == 1) {
+            std::copy(v, v + count, r.begin());
+            return r;
+        }
+        if (mode == 2) {
+            if (ex.allgather(ex.user, v, r.data(), count * 8) != 0)
+                fail(ES_ERR_RUNTIME, "ExchangeError", "allgather callback failed");
+            return r;
+        }
+        double* d = xbuf.as<double>(count * (world + 1));
+        CU(cudaMemcpyAsync(d, v, count * 8, cudaMemcpyHostToDevice, stream));
+        NC(nccl().AllGather(d, d + count, count, ncclFloat64, comm, stream));
+        CU(cudaMemcpyAsync(r.data(), d + count, count * world * 8, cudaMemcpyDeviceToHost, stream));
+        sync();
+        return r;
+    }
+};
+
+struct es_dataset {
+    es_ctx* ctx = nullptr;
+    int64_t n_local = 0, n_global = 0, row_offset = 0, ld = 0;
+    int D = 0;
+    double* X = nullptr;
+    ~es_dataset() {
+        if (X) cudaFree(X);
+    }
+};
+
+struct es_em_state {
+    es_ctx* ctx = nullptr;
+    es_dataset* ds = nullptr;
+    int K = 0, D = 0;
+    es_fit_opts opts{};
+    double reg = 0.0;
+    std::vector<double> S;  // data covariance (D x D)
+    SplitMix64 rng{0};
+    std::vector<double> per_iter;
+    int t = 0;          // E-steps done
+    int iterations = 0; // M-steps kept
+    int collapses = 0;
+    bool converged = false, done = false;
+    double prev = 0.0, last = 0.0;
+};
+
+// ============================================================== helpers
+namespace {
+
+int64_t mstride(int K, int D) { return ModelView::size(K, D); }
+
+void fetch_rows(es_ctx* c, es_dataset* ds, const std::vector<int64_t>& rows, std::vector<double>& out) {
+    const int D = ds->D;
+    const size_t m = rows.size();
+    out.assign(m * D, 0.0);
+    double* d = c->scratch3.as<double>(std::max<size_t>(m * D, 1));
+    bool any = false;
+    for (size_t r = 0; r < m; ++r) {
+        const int64_t li = rows[r] - ds->row_offset;
+        if (li >= 0 && li < ds->n_local) {
+            launch_planar_to_rows(ds->X, ds->ld, D, li, 1, d + r * D, c->stream, c->ls);
+            any = true;
+        }
+    }
+    if (any) {
+        c->check_launch();
+        std::vector<double> tmp(m * D);
+        CU(cudaMemcpyAsync(tmp.data(), d, m * D * 8, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        for (size_t r = 0; r < m; ++r) {
+            const int64_t li = rows[r] - ds->row_offset;
+            if (li >= 0 && li < ds->n_local) std::copy(&tmp[r * D], &tmp[r * D] + D, &out[r * D]);
+        }
+    }
+    // exactly one rank owns each row: the sum is exact
+    c->allreduce_host(out.data(), out.size(), 0, 0);
+}
+
+// Data statistics: mean, S (biased), min/max, non-finite.
+struct DataStats {
+    std::vector<double> mean, S, mn, mx;
+    double nonfinite = 0;
+};
+
+DataStats data_stats(es_ctx* c, es_dataset* ds) {
+    const int D = ds->D;
+    DataStats r;
+    double* out = c->scratch2.as<double>(4 * D);
+    double* scr = c->scratch.as<double>((size_t)D * 1024 * 4);
+    std::vector<double> h(4 * D, 0.0);
+    if (ds->n_local > 0) {
+        launch_col_stats(ds->X, ds->n_local, ds->ld, D, scr, out, c->num_sms, c->stream, c->ls);
+        c->check_launch();
+        CU(cudaMemcpyAsync(h.data(), out, 4 * D * 8, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+    } else {
+        for (int j = 0; j < D; ++j) {
+            h[D + j] = INFINITY;
+            h[2 * D + j] = -INFINITY;
+        }
+    }
+    std::vector<double> sums(2 * D);
+    for (int j = 0; j < D; ++j) {
+        sums[j] = h[j];
+        sums[D + j] = h[3 * D + j];
+    }
+    r.mn.assign(h.begin() + D, h.begin() + 2 * D);
+    r.mx.assign(h.begin() + 2 * D, h.begin() + 3 * D);
+    // rank-ordered sum of column sums keeps the mean identical on every rank
+    std::vector<double> all = c->allgather_host(sums.data(), sums.size());
+    std::vector<double> tot(2 * D, 0.0);
+    for (int g = 0; g < c->world; ++g)
+        for (int j = 0; j < 2 * D; ++j) tot[j] += all[(size_t)g * 2 * D + j];
+    c->allreduce_host(r.mn.data(), D, 0, 1);
+    c->allreduce_host(r.mx.data(), D, 0, 2);
+    for (int j = 0; j < D; ++j) r.nonfinite += tot[D + j];
+    r.mean.resize(D);
+    for (int j = 0; j < D; ++j) r.mean[j] = tot[j] / (double)ds->n_global;
+    r.S.assign((size_t)D * D, 0.0);
+    if (r.nonfinite > 0) return r;
+    // centered second moments about the mean (one unit-weight stats pass)
+    double* dmean = c->scratch2.as<double>(D);
+    CU(cudaMemcpyAsync(dmean, r.mean.data(), D * 8, cudaMemcpyHostToDevice, c->stream));
+    const int SK = stat_k(D);
+    int nblk = 0;
+    double* part = c->partial.as<double>((size_t)em_grid(64, 128, c->num_sms) * 4 * (SK + 1));
+    std::vector<double> loc(SK + 1, 0.0);
+    if (ds->n_local > 0) {
+        launch_unit_stats(ds->X, ds->n_local, ds->ld, D, dmean, part, c->num_sms, &nblk, c->stream, c->ls);
+        double* red = c->stats_local.as<double>(SK + 1);
+        launch_reduce_blocks(part, nblk, SK + 1, red, c->stream, c->ls);
+        c->check_launch();
+        CU(cudaMemcpyAsync(loc.data(), red, (SK + 1) * 8, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+    }
+    std::vector<double> allst = c->allgather_host(loc.data(), SK + 1);
+    std::vector<double> st(SK + 1, 0.0);
+    for (int g = 0; g < c->world; ++g)
+        for (int e = 0; e <= SK; ++e) st[e] += allst[(size_t)g * (SK + 1) + e];
+    const double N = (double)ds->n_global;
+    const double* s1 = &st[1];
+    const double* s2 = &st[1 + D];
+    for (int a = 0; a < D; ++a)
+        for (int b = a; b < D; ++b) {
+            const double v = s2[packed_index(a, b, D)] / N - (s1[a] / N) * (s1[b] / N);
+            r.S[(size_t)a * D + b] = v;
+            r.S[(size_t)b * D + a] = v;
+        }
+    return r;
+}
+
+double default_reg(const std::vector<double>& S, int D) {
+    double tr = 0.0;
+    for (int d = 0; d < D; ++d) tr += S[(size_t)d * D + d];
+    return 1e-6 * tr / D;
+}
+
+// Upload pi/mu/cov into the context model block and derive (Cholesky, W).
+void upload_model(es_ctx* c, double* dmodel, int K, int D, const double* pi, const double* mu, const double* cov) {
+    ModelView mv{K, D, dmodel};
+    CU(cudaMemcpyAsync(mv.pi(), pi, K * 8, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(mv.mu(), mu, (size_t)K * D * 8, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(mv.cov(), cov, (size_t)K * D * D * 8, cudaMemcpyHostToDevice, c->stream));
+    IterStatus* st = c->status.as<IterStatus>(1);
+    CU(cudaMemsetAsync(st, 0, sizeof(IterStatus), c->stream));
+    launch_derive(dmodel, D, K, st, c->stream, c->ls);
+    c->check_launch();
+    CU(cudaMemcpyAsync(c->h_status, st, sizeof(IterStatus), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    if (c->h_status->not_pd)
+        fail(ES_ERR_NUMERIC, "SingularCovariance", "a covariance matrix is not positive definite");
+}
+
+void check_params(const es_gmm_params* p, int D) {
+    if (!p || !p->weights || !p->means || !p->covariances) fail(ES_ERR_DATA, "InvalidModel", "null parameters");
+    if (p->K < 1 || p->K > 128) fail(ES_ERR_DATA, "InvalidModel", "K must be in [1,128]");
+    if (p->D != D) fail(ES_ERR_DATA, "DimensionMismatch", "model dimension does not match the data");
+    for (int k = 0; k < p->K; ++k)
+        if (!(p->weights[k] >= 0.0) || !std::isfinite(p->weights[k]))
+            fail(ES_ERR_DATA, "InvalidModel", "weights must be finite and non-negative");
+}
+
+double* model_for(es_ctx* c, const es_gmm_params* p, int D) {
+    check_params(p, D);
+    double* m = c->model.as<double>(mstride(p->K, D));
+    upload_model(c, m, p->K, D, p->weights, p->means, p->covariances);
+    return m;
+}
+
+// Output staging: device pointers are written directly, host pointers via scratch.
+template <class T>
+struct Out {
+    T* user;
+    T* dev;
+    size_t count;
+    DevBuf* buf;
+    Out(T* u, size_t n, DevBuf& b) : user(u), dev(nullptr), count(n), buf(&b) {
+        if (!u) return;
+        if (is_device_ptr(u)) dev = u;
+        else dev = b.as<T>(std::max<size_t>(n, 1));
+    }
+    void finish(cudaStream_t s) {
+        if (user && dev != user && count) CU(cudaMemcpyAsync(user, dev, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+    }
+};
+
+double run_score(es_ctx* c, es_dataset* ds, const double* dmodel, int K, ScoreOut o) {
+    const int D = ds->D;
+    double* bs = c->scratch.as<double>((size_t)2 * score_grid(D, K, c->num_sms) + 2);
+    double loc = 0.0;
+    if (ds->n_local > 0) {
+        int nblk = 0;
+        c->t_begin();
+        launch_score(ds->X, ds->n_local, ds->ld, D, K, dmodel, o, bs, c->num_sms, &nblk, c->stream, c->ls);
+        c->t_end(c->score_ms, c->score_launches);
+        double* red = c->scratch2.as<double>(2);
+        launch_reduce_blocks(bs, nblk, 2, red, c->stream, c->ls);
+        c->check_launch();
+        double h[2];
+        CU(cudaMemcpyAsync(h, red, 16, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        loc = h[0];
+    }
+    std::vector<double> all = c->allgather_host(&loc, 1);
+    double tot = 0.0;
+    for (double v : all) tot += v;
+    return tot;
+}
+
+// Exact order statistic (global rank r) of FP64 keys by 8-bit radix select.
+double radix_select(es_ctx* c, const double* dkeys, int64_t n, int64_t r) {
+    unsigned long long* hist = c->hist.as<unsigned long long>(256);
+    uint64_t prefix = 0, mask = 0;
+    std::vector<long long> h(256);
+    for (int pass = 0; pass < 8; ++pass) {
+        const int shift = 56 - 8 * pass;
+        launch_hist8(dkeys, n, shift, mask, prefix, hist, c->num_sms, c->stream, c->ls);
+        c->check_launch();
+        CU(cudaMemcpyAsync(h.data(), hist, 256 * 8, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        c->allreduce_host(h.data(), 256, 1, 0);
+        long long cum = 0;
+        int digit = 255;
+        for (int b = 0; b < 256; ++b) {
+            if (cum + h[b] > r) {
+                digit = b;
+                break;
+            }
+            cum += h[b];
+        }
+        r -= cum;
+        prefix |= (uint64_t)digit << shift;
+        mask |= (uint64_t)0xFF << shift;
+    }
+    const uint64_t u = (prefix >> 63) ? (prefix & 0x7FFFFFFFFFFFFFFFull) : ~prefix;
+    double v;
+    std::memcpy(&v, &u, 8);
+    return v;
+}
+
+// ---------------------------------------------------------------- EM core
+void em_init_model(es_em_state* st, const es_gmm_params* init, const DataStats& dsx) {
+    es_ctx* c = st->ctx;
+    es_dataset* ds = st->ds;
+    const int K = st->K, D = st->D;
+    std::vector<double> pi(K), mu((size_t)K * D), cov((size_t)K * D * D);
+    if (st->opts.init == ES_INIT_GIVEN) {
+        check_params(init, D);
+        if (init->K != K) fail(ES_ERR_DATA, "DimensionMismatch", "init K differs from requested K");
+        std::copy(init->weights, init->weights + K, pi.begin());
+        std::copy(init->means, init->means + (size_t)K * D, mu.begin());
+        std::copy(init->covariances, init->covariances + (size_t)K * D * D, cov.begin());
+    } else {
+        std::vector<int64_t> rows;
+        if (st->opts.init == ES_INIT_KMEANSPP) {
+            // k-means++ (DESIGN.md): first centre uniform; then D^2-weighted draws,
+            // cumulative sum over global rows in chunk order (4096-row chunks).
+            rows.push_back((int64_t)st->rng.below((uint64_t)ds->n_global));
+            const int64_t CH = 4096;
+            const int64_t nlc = (ds->n_local + CH - 1) / CH;
+            double* d2 = c->scratch3.as<double>(std::max<int64_t>(ds->n_local, 1) + nlc + 8);
+            double* parts = d2 + std::max<int64_t>(ds->n_local, 1);
+            double* dcen = c->scratch2.as<double>(D);
+            std::vector<double> cen;
+            for (int j = 1; j < K; ++j) {
+                fetch_rows(c, ds, {rows.back()}, cen);
+                CU(cudaMemcpyAsync(dcen, cen.data(), D * 8, cudaMemcpyHostToDevice, c->stream));
+                launch_kpp_update(ds->X, ds->n_local, ds->ld, D, dcen, d2, parts, j == 1, c->stream, c->ls);
+                c->check_launch();
+                std::vector<double> hp(nlc);
+                if (nlc) CU(cudaMemcpyAsync(hp.data(), parts, nlc * 8, cudaMemcpyDeviceToHost, c->stream));
+                c->sync();
+                double loc = 0.0;
+                for (double v : hp) loc += v;
+                std::vector<double> all = c->allgather_host(&loc, 1);
+                double total = 0.0;
+                for (double v : all) total += v;
+                const double u = st->rng.uniform() * total;
+                int64_t pick = -1;
+                if (total > 0.0) {
+                    // owner rank of the crossing point locates the row; others report -1
+                    double before = 0.0;
+                    for (int g = 0; g < c->rank; ++g) before += all[g];
+                    double found = -1.0;
+                    if (u >= before && u < before + all[c->rank]) {
+                        double acc = before;
+                        int64_t ch = 0;
+                        for (; ch < nlc; ++ch) {
+                            if (acc + hp[ch] > u) break;
+                            acc += hp[ch];
+                        }
+                        if (ch == nlc) ch = nlc - 1;
+                        const int64_t r0 = ch * CH, nr = std::min(CH, ds->n_local - r0);
+                        std::vector<double> seg(nr);
+                        CU(cudaMemcpyAsync(seg.data(), d2 + r0, nr * 8, cudaMemcpyDeviceToHost, c->stream));
+                        c->sync();
+                        int64_t li = r0 + nr - 1;
+                        for (int64_t q = 0; q < nr; ++q) {
+                            acc += seg[q];
+                            if (acc > u) {
+                                li = r0 + q;
+                                break;
+                            }
+                        }
+                        found = (double)(ds->row_offset + li);
+                    }
+                    c->allreduce_host(&found, 1, 0, 2);
+                    pick = (int64_t)found;
+                }
+                if (pick < 0) pick = (int64_t)st->rng.below((uint64_t)ds->n_global);
+                rows.push_back(pick);
+            }
+        } else {
+            while ((int)rows.size() < K) {
+                const int64_t r = (int64_t)st->rng.below((uint64_t)ds->n_global);
+                if (std::find(rows.begin(), rows.end(), r) == rows.end()) rows.push_back(r);
+            }
+        }
+        std::vector<double> X0;
+        fetch_rows(c, ds, rows, X0);
+        for (int k = 0; k < K; ++k) {
+            pi[k] = 1.0 / K;
+            std::copy(&X0[(size_t)k * D], &X0[(size_t)k * D] + D, &mu[(size_t)k * D]);
+            for (int a = 0; a < D; ++a)
+                for (int b = 0; b < D; ++b)
+                    cov[(size_t)k * D * D + a * D + b] = dsx.S[(size_t)a * D + b] + (a == b ? st->reg : 0.0);
+        }
+    }
+    double* m = c->model.as<double>(mstride(K, D));
+    upload_model(c, m, K, D, pi.data(), mu.data(), cov.data());
+}
+
+void em_begin(es_em_state* st, const es_gmm_params* init) {
+    es_ctx* c = st->ctx;
+    es_dataset* ds = st->ds;
+    const int K = st->K, D = st->D;
+    if (K < 1 || ds->n_global < K) fail(ES_ERR_DATA, "TooFewPoints", "fit_em requires N >= K >= 1");
+    if (K > 128) fail(ES_ERR_DATA, "InvalidModel", "K must be <= 128");
+    if (st->opts.max_iter < 0) fail(ES_ERR_DATA, "RangeViolation", "max_iter must be >= 0");
+    DataStats dsx = data_stats(c, ds);
+    if (dsx.nonfinite > 0) fail(ES_ERR_DATA, "NonFiniteInput", "X contains non-finite entries");
+    if (K > 1) {
+        bool deg = true;
+        for (int j = 0; j < D; ++j)
+            if (dsx.mn[j] != dsx.mx[j]) deg = false;
+        if (deg) fail(ES_ERR_DATA, "DegenerateData", "all points identical and K > 1");
+    }
+    st->S = dsx.S;
+    st->reg = st->opts.reg < 0 ? default_reg(dsx.S, D) : st->opts.reg;
+    st->rng = SplitMix64(st->opts.seed);
+    em_init_model(st, init, dsx);
+}
+
+// One EM iteration; returns true when the loop must stop.
+bool em_iterate(es_em_state* st) {
+    es_ctx* c = st->ctx;
+    es_dataset* ds = st->ds;
+    const int K = st->K, D = st->D;
+    const int NE1 = stat_total(D, K);
+    double* dmodel = c->model.as<double>(mstride(K, D));
+    double* backup = c->model_backup.as<double>(mstride(K, D));
+    CU(cudaMemcpyAsync(backup, dmodel, mstride(K, D) * 8, cudaMemcpyDeviceToDevice, c->stream));
+    double* loc = c->stats_local.as<double>(NE1);
+    bool whitened = true;
+    if (ds->n_local > 0) {
+        int nblk = 0;
+        double* part = c->partial.as<double>((size_t)em_grid(D, K, c->num_sms) * NE1);
+        c->t_begin();
+        launch_em_pass(ds->X, ds->n_local, ds->ld, D, K, dmodel, part, c->num_sms, &nblk, &whitened, c->stream, c->ls);
+        c->t_end(c->em_ms, c->em_launches);
+        launch_reduce_blocks(part, nblk, NE1, loc, c->stream, c->ls);
+    } else {
+        CU(cudaMemsetAsync(loc, 0, NE1 * 8, c->stream));
+        whitened = em_path(D, K) != EmPath::Generic;
+    }
+    double* all = c->stats_all.as<double>((size_t)NE1 * c->world);
+    c->allgather(loc, all, NE1);
+    IterStatus* dst = c->status.as<IterStatus>(1);
+    CU(cudaMemsetAsync(dst, 0, sizeof(IterStatus), c->stream));
+    launch_finalize(all, c->world, D, K, ds->n_global, st->reg, whitened, dmodel, dst, nullptr, st->t, c->stream,
+                    c->ls);
+    c->check_launch();
+    CU(cudaMemcpyAsync(c->h_status, dst, sizeof(IterStatus), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    const IterStatus s = *c->h_status;
+    const double cur = s.logL;
+    st->per_iter.push_back(cur);
+    st->last = cur;
+    const int t = st->t++;
+    if (t >= 1 && std::fabs(cur - st->prev) < st->opts.tol * (1.0 + std::fabs(cur))) {
+        // converged: theta_t (before this M-step) is returned, final logL = logL_t
+        CU(cudaMemcpyAsync(dmodel, backup, mstride(K, D) * 8, cudaMemcpyDeviceToDevice, c->stream));
+        c->sync();
+        st->converged = true;
+        return true;
+    }
+    st->prev = cur;
+    if (s.not_pd) fail(ES_ERR_NUMERIC, "SingularCovariance", "updated covariance is not positive definite");
+    if (s.collapse_lo || s.collapse_hi) {
+        // reseed mean at a uniform data row, covariance to the
+        // data covariance (+reg), weight 1/K then renormalise; at most twice.
+        ModelView mv{K, D, dmodel};
+        std::vector<double> pi(K), mu((size_t)K * D), cov((size_t)K * D * D);
+        CU(cudaMemcpyAsync(pi.data(), mv.pi(), K * 8, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaMemcpyAsync(mu.data(), mv.mu(), (size_t)K * D * 8, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaMemcpyAsync(cov.data(), mv.cov(), (size_t)K * D * D * 8, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        for (int k = 0; k < K; ++k) {
+            const bool col = k < 64 ? ((s.collapse_lo >> k) & 1) : ((s.collapse_hi >> (k - 64)) & 1);
+            if (!col) continue;
+            if (++st->collapses > 2) fail(ES_ERR_NUMERIC, "RepeatedCollapse", "component collapsed more than twice");
+            const int64_t r = (int64_t)st->rng.below((uint64_t)ds->n_global);
+            std::vector<double> row;
+            fetch_rows(c, ds, {r}, row);
+            std::copy(row.begin(), row.end(), &mu[(size_t)k * D]);
+            for (int a = 0; a < D; ++a)
+                for (int b = 0; b < D; ++b)
+                    cov[(size_t)k * D * D + a * D + b] = st->S[(size_t)a * D + b] + (a == b ? st->reg : 0.0);
+            pi[k] = 1.0 / K;
+        }
+        double z = 0.0;
+        for (int k = 0; k < K; ++k) z += pi[k];
+        for (int k = 0; k < K; ++k) pi[k] /= z;
+        upload_model(c, dmodel, K, D, pi.data(), mu.data(), cov.data());
+    }
+    st->iterations = t + 1;
+    return false;
+}
+
+}  // namespace
+
+// ================================================================= C ABI
+extern "C" {
+
+const char* es_last_error_name(void) { return g_name.c_str(); }
+const char* es_last_error_message(void) { return g_msg.c_str(); }
+const char* es_version(void) { return "eventscope-b200 0.1.0 (sm_100a)"; }
+
+static void ctx_common(es_ctx* c, int device) {
+    c->device = device;
+    CU(cudaSetDevice(device));
+    CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CU(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    CU(cudaMallocHost(&c->h_status, sizeof(IterStatus)));
+}
+
+int es_ctx_create(int device, es_ctx** out) {
+    return guard([&] {
+        auto c = std::make_unique<es_ctx>();
+        ctx_common(c.get(), device);
+        *out = c.release();
+    });
+}
+
+int es_nccl_unique_id(unsigned char id[128]) {
+    return guard([&] {
+        ncclUniqueId u;
+        NC(nccl().GetUniqueId(&u));
+        static_assert(sizeof(u) == 128, "nccl id size");
+        std::memcpy(id, &u, 128);
+    });
+}
+
+int es_ctx_create_nccl(int device, int rank, int world, const unsigned char id[128], es_ctx** out) {
+    return guard([&] {
+        if (world < 1 || rank < 0 || rank >= world) fail(ES_ERR_DATA, "RangeViolation", "bad rank/world");
+        auto c = std::make_unique<es_ctx>();
+        ctx_common(c.get(), device);
+        c->rank = rank;
+        c->world = world;
+        if (world > 1) {
+            ncclUniqueId u;
+            std::memcpy(&u, id, 128);
+            NC(nccl().CommInitRank(&c->comm, world, u, rank));
+            c->mode = 1;
+        }
+        *out = c.release();
+    });
+}
+
+int es_ctx_create_exchange(int device, int rank, int world, const es_exchange* ex, es_ctx** out) {
+    return guard([&] {
+        if (world < 1 || rank < 0 || rank >= world) fail(ES_ERR_DATA, "RangeViolation", "bad rank/world");
+        if (world > 1 && (!ex || !ex->allgather || !ex->allreduce))
+            fail(ES_ERR_DATA, "InvalidExchange", "exchange callbacks required");
+        auto c = std::make_unique<es_ctx>();
+        ctx_common(c.get(), device);
+        c->rank = rank;
+        c->world = world;
+        if (world > 1) {
+            c->ex = *ex;
+            c->mode = 2;
+        }
+        *out = c.release();
+    });
+}
+
+int es_ctx_destroy(es_ctx* c) {
+    return guard([&] {
+        if (!c) return;
+        cudaSetDevice(c->device);
+        cudaStreamSynchronize(c->stream);
+        if (c->comm) nccl().CommDestroy(c->comm);
+        if (c->h_status) cudaFreeHost(c->h_status);
+        if (c->ev0) cudaEventDestroy(c->ev0);
+        if (c->ev1) cudaEventDestroy(c->ev1);
+        cudaStreamDestroy(c->stream);
+        delete c;
+    });
+}
+
+int es_ctx_stream(es_ctx* c, void** stream) {
+    return guard([&] { *stream = (void*)c->stream; });
+}
+
+int es_ctx_launch_count(es_ctx* c, int64_t* count) {
+    return guard([&] { *count = c->ls.launches; });
+}
+
+int es_ctx_set_timing(es_ctx* c, int enable) {
+    return guard([&] {
+        CU(cudaSetDevice(c->device));
+        if (enable && !c->ev0) {
+            CU(cudaEventCreate(&c->ev0));
+            CU(cudaEventCreate(&c->ev1));
+        }
+        c->timing = enable != 0;
+        c->em_ms = c->score_ms = 0.0;
+        c->em_launches = c->score_launches = 0;
+    });
+}
+
+int es_ctx_kernel_time(es_ctx* c, int which, double* ms, int64_t* launches) {
+    return guard([&] {
+        *ms = which == 0 ? c->em_ms : c->score_ms;
+        *launches = which == 0 ? c->em_launches : c->score_launches;
+    });
+}
+
+// -------------------------------------------------------------- dataset
+static void finish_dataset(es_ctx* c, es_dataset* ds) {
+    double nl = (double)ds->n_local;
+    std::vector<double> all = c->allgather_host(&nl, 1);
+    int64_t off = 0, tot = 0;
+    for (int g = 0; g < c->world; ++g) {
+        if (g < c->rank) off += (int64_t)all[g];
+        tot += (int64_t)all[g];
+    }
+    ds->row_offset = off;
+    ds->n_global = tot;
+}
+
+int es_dataset_create(es_ctx* c, const double* X, int64_t n_local, int32_t D, int64_t row_stride,
+                      int64_t col_stride, es_dataset** out) {
+    return guard([&] {
+        if (D < 1 || D > 64) fail(ES_ERR_DATA, "DimensionMismatch", "D must be in [1,64]");
+        if (n_local < 0) fail(ES_ERR_DATA, "RangeViolation", "negative row count");
+        CU(cudaSetDevice(c->device));
+        auto ds = std::make_unique<es_dataset>();
+        ds->ctx = c;
+        ds->n_local = n_local;
+        ds->D = D;
+        ds->ld = plane_ld(std::max<int64_t>(n_local, 1));
+        CU(cudaMalloc(&ds->X, (size_t)ds->ld * D * 8));
+        if (n_local > 0) {
+            if (!X) fail(ES_ERR_DATA, "InvalidInput", "null matrix");
+            const bool dev = is_device_ptr(X);
+            std::vector<double> packed;
+            if (!(row_stride == D && col_stride == 1) && !(row_stride == 1 && col_stride >= n_local)) {
+                if (dev) fail(ES_ERR_DATA, "UnsupportedLayout", "device input must be row- or column-major");
+                packed.resize((size_t)n_local * D);
+                for (int64_t i = 0; i < n_local; ++i)
+                    for (int j = 0; j < D; ++j) packed[(size_t)i * D + j] = X[i * row_stride + (int64_t)j * col_stride];
+                X = packed.data();
+                row_stride = D;
+                col_stride = 1;
+            }
+            if (row_stride == 1) {
+                CU(cudaMemcpy2DAsync(ds->X, ds->ld * 8, X, col_stride * 8, n_local * 8, D, cudaMemcpyDefault,
+                                     c->stream));
+            } else {
+                const int64_t chunk = std::max<int64_t>(1, (64ll << 20) / (8 * D));
+                double* stage = c->scratch3.as<double>((size_t)std::min(chunk, n_local) * D);
+                for (int64_t r0 = 0; r0 < n_local; r0 += chunk) {
+                    const int64_t nr = std::min(chunk, n_local - r0);
+                    CU(cudaMemcpyAsync(stage, X + r0 * D, (size_t)nr * D * 8, cudaMemcpyDefault, c->stream));
+                    launch_rows_to_planar(stage, nr, D, ds->X, ds->ld, r0, c->stream, c->ls);
+                    c->check_launch();
+                }
+            }
+            c->sync();
+        }
+        finish_dataset(c, ds.get());
+        *out = ds.release();
+    });
+}
+
+// SYN-v1 true model: host SplitMix64 stream, same algorithm as
+// the oracle's eso_syn_model; rows come from the device Philox generator.
+static void syn_true_model(uint64_t seed, int D, int K, std::vector<double>& cum, std::vector<double>& mu,
+                           std::vector<double>& chol) {
+    SplitMix64 rng(seed ^ 0x53594E2D76310000ull);
+    auto normal = [&]() {
+        const double u1 = 1.0 - rng.uniform(), u2 = rng.uniform();
+        return std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * M_PI * u2);
+    };
+    double z = 0.0;
+    for (int k = 0; k < K; ++k) z += (double)(k + 1);
+    cum.resize(K);
+    double acc = 0.0;
+    for (int k = 0; k < K; ++k) {
+        acc += (double)(k + 1) / z;
+        cum[k] = acc;
+    }
+    mu.resize((size_t)K * D);
+    chol.assign((size_t)K * D * D, 0.0);
+    std::vector<double> B((size_t)D * D), Sg((size_t)D * D);
+    for (int k = 0; k < K; ++k) {
+        for (int d = 0; d < D; ++d) mu[(size_t)k * D + d] = -3.0 + 6.0 * rng.uniform();
+        for (auto& b : B) b = normal();
+        for (int a = 0; a < D; ++a)
+            for (int c = 0; c < D; ++c) {
+                double s = 0.0;
+                for (int p = 0; p < D; ++p) s += B[(size_t)a * D + p] * B[(size_t)c * D + p];
+                Sg[(size_t)a * D + c] = s / D + (a == c ? 0.05 : 0.0);
+            }
+        double* L = &chol[(size_t)k * D * D];
+        for (int j = 0; j < D; ++j) {
+            double s = Sg[(size_t)j * D + j];
+            for (int p = 0; p < j; ++p) s -= L[j * D + p] * L[j * D + p];
+            L[j * D + j] = std::sqrt(s);
+            for (int i = j + 1; i < D; ++i) {
+                double t = Sg[(size_t)i * D + j];
+                for (int p = 0; p < j; ++p) t -= L[i * D + p] * L[j * D + p];
+                L[i * D + j] = t / L[j * D + j];
+            }
+        }
+    }
+}
+
+int es_dataset_generate(es_ctx* c, uint64_t seed, int64_t n_global, int32_t D, int32_t K_true, es_dataset** out) {
+    return guard([&] {
+        if (D < 1 || D > 64) fail(ES_ERR_DATA, "DimensionMismatch", "D must be in [1,64]");
+        if (K_true < 1 || n_global < 0) fail(ES_ERR_DATA, "RangeViolation", "bad generator shape");
+        CU(cudaSetDevice(c->device));
+        auto ds = std::make_unique<es_dataset>();
+        ds->ctx = c;
+        ds->D = D;
+        const int64_t r0 = n_global * c->rank / c->world, r1 = n_global * (c->rank + 1) / c->world;
+        ds->n_local = r1 - r0;
+        ds->ld = plane_ld(std::max<int64_t>(ds->n_local, 1));
+        CU(cudaMalloc(&ds->X, (size_t)ds->ld * D * 8));
+        std::vector<double> cum, mu, chol;
+        syn_true_model(seed, D, K_true, cum, mu, chol);
+        std::vector<double> blob;
+        blob.insert(blob.end(), cum.begin(), cum.end());
+        blob.insert(blob.end(), mu.begin(), mu.end());
+        blob.insert(blob.end(), chol.begin(), chol.end());
+        double* dm = c->scratch2.as<double>(blob.size());
+        CU(cudaMemcpyAsync(dm, blob.data(), blob.size() * 8, cudaMemcpyHostToDevice, c->stream));
+        launch_synth(ds->X, ds->ld, ds->n_local, r0, D, K_true, dm, seed, c->stream, c->ls);
+        c->check_launch();
+        c->sync();
+        finish_dataset(c, ds.get());
+        *out = ds.release();
+    });
+}
+
+int es_dataset_destroy(es_dataset* ds) {
+    return guard([&] { delete ds; });
+}
+
+int es_dataset_info(es_dataset* ds, int64_t* n_local, int64_t* n_global, int64_t* row_offset, int32_t* D) {
+    return guard([&] {
+        if (n_local) *n_local = ds->n_local;
+        if (n_global) *n_global = ds->n_global;
+        if (row_offset) *row_offset = ds->row_offset;
+        if (D) *D = ds->D;
+    });
+}
+
+int es_dataset_read_rows(es_dataset* ds, int64_t row0, int64_t n, double* out) {
+    return guard([&] {
+        if (row0 < 0 || n < 0 || row0 + n > ds->n_local) fail(ES_ERR_DATA, "RangeViolation", "rows out of range");
+        es_ctx* c = ds->ctx;
+        if (n == 0) return;
+        double* d = c->out_scratch.as<double>((size_t)n * ds->D);
+        launch_planar_to_rows(ds->X, ds->ld, ds->D, row0, n, d, c->stream, c->ls);
+        c->check_launch();
+        CU(cudaMemcpyAsync(out, d, (size_t)n * ds->D * 8, cudaMemcpyDefault, c->stream));
+        c->sync();
+    });
+}
+
+// ------------------------------------------------------------------ fit
+int es_gmm_em_begin(es_ctx* c, es_dataset* ds, int32_t K, const es_fit_opts* opts, const es_gmm_params* init,
+                    es_em_state** out) {
+    return guard([&] {
+        CU(cudaSetDevice(c->device));
+        if (!opts) fail(ES_ERR_DATA, "InvalidOptions", "null options");
+        auto st = std::make_unique<es_em_state>();
+        st->ctx = c;
+        st->ds = ds;
+        st->K = K;
+        st->D = ds->D;
+        st->opts = *opts;
+        em_begin(st.get(), init);
+        *out = st.release();
+    });
+}
+
+int es_gmm_em_step(es_em_state* st, int32_t n_iter, int32_t* done) {
+    return guard([&] {
+        CU(cudaSetDevice(st->ctx->device));
+        for (int i = 0; i < n_iter && !st->done; ++i) {
+            if (st->t >= st->opts.max_iter) {
+                st->done = true;
+                break;
+            }
+            if (em_iterate(st)) st->done = true;
+        }
+        if (st->t >= st->opts.max_iter) st->done = true;
+        if (done) *done = st->done ? 1 : 0;
+    });
+}
+
+int es_gmm_em_end(es_em_state* st, es_gmm_params* out, es_fit_report* rep, double* per_iter) {
+    return guard([&] {
+        es_ctx* c = st->ctx;
+        CU(cudaSetDevice(c->device));
+        const int K = st->K, D = st->D;
+        double* dmodel = c->model.as<double>(mstride(K, D));
+        double final_ll = st->last;
+        if (!st->converged) final_ll = run_score(c, st->ds, dmodel, K, ScoreOut{});
+        if (out) {
+            if (out->K != K || out->D != D) fail(ES_ERR_DATA, "DimensionMismatch", "output params shape");
+            ModelView mv{K, D, dmodel};
+            CU(cudaMemcpyAsync(out->weights, mv.pi(), K * 8, cudaMemcpyDeviceToHost, c->stream));
+            CU(cudaMemcpyAsync(out->means, mv.mu(), (size_t)K * D * 8, cudaMemcpyDeviceToHost, c->stream));
+            CU(cudaMemcpyAsync(out->covariances, mv.cov(), (size_t)K * D * D * 8, cudaMemcpyDeviceToHost, c->stream));
+            c->sync();
+        }
+        if (rep) {
+            rep->iterations = st->iterations;
+            rep->final_log_likelihood = final_ll;
+            rep->converged = st->converged ? 1 : 0;
+            rep->seed = st->opts.seed;
+            rep->n_per_iter = (int32_t)st->per_iter.size();
+            rep->collapses = st->collapses;
+            rep->reg_used = st->reg;
+        }
+        if (per_iter) std::copy(st->per_iter.begin(), st->per_iter.end(), per_iter);
+    });
+}
+
+int es_gmm_em_free(es_em_state* st) {
+    return guard([&] { delete st; });
+}
+
+int es_gmm_fit(es_ctx* c, es_dataset* ds, int32_t K, const es_fit_opts* opts, const es_gmm_params* init,
+               es_gmm_params* out, es_fit_report* rep, double* per_iter) {
+    es_em_state* st = nullptr;
+    int s = es_gmm_em_begin(c, ds, K, opts, init, &st);
+    if (s) return s;
+    int32_t done = 0;
+    s = es_gmm_em_step(st, opts->max_iter, &done);
+    if (!s) s = es_gmm_em_end(st, out, rep, per_iter);
+    delete st;
+    return s;
+}
+
+// ---------------------------------------------------------------- score
+int es_gmm_score(es_ctx* c, es_dataset* ds, const es_gmm_params* p, double* ll, int32_t* predict, int32_t* best_k,
+                 double* best_logdens, double* total_ll) {
+    return guard([&] {
+        CU(cudaSetDevice(c->device));
+        double* m = model_for(c, p, ds->D);
+        const size_t n = ds->n_local;
+        Out<double> o_ll(ll, n, c->o1), o_bl(best_logdens, n, c->o2);
+        Out<int32_t> o_pr(predict, n, c->o3), o_bk(best_k, n, c->o4);
+        ScoreOut o;
+        o.ll = o_ll.dev;
+        o.best_ld = o_bl.dev;
+        o.predict = o_pr.dev;
+        o.best_k = o_bk.dev;
+        const double tot = run_score(c, ds, m, p->K, o);
+        o_ll.finish(c->stream);
+        o_bl.finish(c->stream);
+        o_pr.finish(c->stream);
+        o_bk.finish(c->stream);
+        c->sync();
+        if (total_ll) *total_ll = tot;
+    });
+}
+
+int es_gmm_responsibilities(es_ctx* c, es_dataset* ds, const es_gmm_params* p, double* gamma) {
+    return guard([&] {
+        CU(cudaSetDevice(c->device));
+        double* m = model_for(c, p, ds->D);
+        Out<double> o_g(gamma, (size_t)ds->n_local * p->K, c->o1);
+        ScoreOut o;
+        o.gamma = o_g.dev;
+        run_score(c, ds, m, p->K, o);
+        o_g.finish(c->stream);
+        c->sync();
+    });
+}
+
+static void single_event(es_ctx* c, const es_gmm_params* p, const double* x, std::vector<double>& lnk, double* ll) {
+    check_params(p, p->D);
+    const int D = p->D, K = p->K;
+    double* m = model_for(c, p, D);
+    double* dx = c->scratch3.as<double>(D + (size_t)K + 8);
+    double* dl = dx + D;
+    double* dll = dl + K;
+    CU(cudaMemcpyAsync(dx, x, D * 8, cudaMemcpyHostToDevice, c->stream));
+    ScoreOut o;
+    o.lnk = dl;
+    o.ll = dll;
+    double* bs = c->scratch.as<double>((size_t)2 * score_grid(D, K, c->num_sms) + 2);
+    int nblk = 0;
+    launch_score(dx, 1, 1, D, K, m, o, bs, c->num_sms, &nblk, c->stream, c->ls);
+    c->check_launch();
+    lnk.resize(K);
+    CU(cudaMemcpyAsync(lnk.data(), dl, K * 8, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaMemcpyAsync(ll, dll, 8, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+}
+
+int es_gmm_component_log_density(es_ctx* c, const es_gmm_params* p, const double* x, int32_t k, double* out) {
+    return guard([&] {
+        CU(cudaSetDevice(c->device));
+        if (!p || k < 0 || k >= p->K) fail(ES_ERR_DATA, "DimensionMismatch", "component index out of range");
+        std::vector<double> lnk;
+        double ll;
+        single_event(c, p, x, lnk, &ll);
+        *out = lnk[k];
+    });
+}
+
+int es_gmm_mixture_log_density(es_ctx* c, const es_gmm_params* p, const double* x, double* out) {
+    return guard([&] {
+        CU(cudaSetDevice(c->device));
+        std::vector<double> lnk;
+        single_event(c, p, x, lnk, out);
+    });
+}
+
+// --------------------------------------------------------------- detect
+int es_gmm_detect(es_ctx* c, es_dataset* ds, const es_gmm_params* p, double log_delta, int32_t mode, uint8_t* flags,
+                  int32_t* best_k, double* best_logdens, int64_t* anomaly_indices, int64_t* n_local_flagged,
+                  int64_t* n_flagged) {
+    return guard([&] {
+        CU(cudaSetDevice(c->device));
+        if (mode != 0 && mode != 1) fail(ES_ERR_DATA, "RangeViolation", "mode must be 0 or 1");
+        double* m = model_for(c, p, ds->D);
+        const size_t n = ds->n_local;
+        uint8_t* dflags = flags && is_device_ptr(flags) ? flags : c->o5.as<uint8_t>(std::max<size_t>(n, 1));
+        Out<int32_t> o_bk(best_k, n, c->o2);
+        Out<double> o_bl(best_logdens, n, c->o3);
+        Out<int64_t> o_idx(anomaly_indices, n, c->o4);
+        ScoreOut o;
+        o.flags = dflags;
+        o.best_k = o_bk.dev;
+        o.best_ld = o_bl.dev;
+        o.log_delta = log_delta;
+        o.mode = mode;
+        run_score(c, ds, m, p->K, o);
+        int64_t* cnt = c->scratch2.as<int64_t>((n + 4095) / 4096 + 2);
+        int64_t* dcount = cnt + (n + 4095) / 4096 + 1;
+        launch_compact(dflags, n, ds->row_offset, cnt, o_idx.dev, dcount, c->stream, c->ls);
+        c->check_launch();
+        int64_t local = 0;
+        CU(cudaMemcpyAsync(&local, dcount, 8, cudaMemcpyDeviceToHost, c->stream));
+        if (flags && dflags != flags) CU(cudaMemcpyAsync(flags, dflags, n, cudaMemcpyDeviceToHost, c->stream));
+        o_bk.finish(c->stream);
+        o_bl.finish(c->stream);
+        c->sync();
+        if (o_idx.user && o_idx.dev != o_idx.user && local)
+            CU(cudaMemcpyAsync(o_idx.user, o_idx.dev, local * 8, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        if (n == 0) local = 0;
+        if (n_local_flagged) *n_local_flagged = local;
+        long long g = local;
+        c->allreduce_host(&g, 1, 1, 0);
+        if (n_flagged) *n_flagged = g;
+    });
+}
+
+int es_gmm_calibrate(es_ctx* c, es_dataset* ds, const es_gmm_params* p, int64_t n_train, double q, int32_t mode,
+                     double* delta, double* log_delta) {
+    return guard([&] {
+        CU(cudaSetDevice(c->device));
+        if (n_train < 1) fail(ES_ERR_DATA, "EmptyTraining", "training split is empty");
+        if (n_train > ds->n_global) fail(ES_ERR_DATA, "RangeViolation", "n_train exceeds the dataset");
+        if (!(q > 0.0 && q < 1.0)) fail(ES_ERR_DATA, "RangeViolation", "q must be in (0,1)");
+        if (mode != 0 && mode != 1) fail(ES_ERR_DATA, "RangeViolation", "mode must be 0 or 1");
+        double* m = model_for(c, p, ds->D);
+        const int64_t nloc = std::max<int64_t>(0, std::min(ds->n_local, n_train - ds->row_offset));
+        double* keys = c->out_scratch.as<double>(std::max<int64_t>(nloc, 1));
+        if (nloc > 0) {  // the train rows are the first nloc local rows (planes keep their stride)
+            ScoreOut o;
+            if (mode == 1) o.ll = keys;
+            else o.best_ld = keys;
+            int nblk = 0;
+            double* bs = c->scratch.as<double>((size_t)2 * score_grid(ds->D, p->K, c->num_sms) + 2);
+            launch_score(ds->X, nloc, ds->ld, ds->D, p->K, m, o, bs, c->num_sms, &nblk, c->stream, c->ls);
+            c->check_launch();
+        }
+        // q-quantile, linear interpolation between order statistics, h = (n-1) q
+        const double h = (double)(n_train - 1) * q;
+        const int64_t lo = (int64_t)std::floor(h);
+        const int64_t hi = std::min<int64_t>(lo + 1, n_train - 1);
+        const double vlo = radix_select(c, keys, nloc, lo);
+        const double vhi = hi == lo ? vlo : radix_select(c, keys, nloc, hi);
+        const double dlo = std::exp(vlo), dhi = std::exp(vhi);
+        const double frac = h - (double)lo;
+        const double d = dlo + frac * (dhi - dlo);
+        *delta = d;
+        // one shared log(delta); exact endpoints keep their log
+        *log_delta = (d == dlo) ? vlo : (d == dhi) ? vhi : std::log(d);
+    });
+}
+
+int es_gmm_select_k_bic(es_ctx* c, es_dataset* ds, const int32_t* k_range, int32_t n_k, const es_fit_opts* opts,
+                        int32_t* best_k, double* bic) {
+    return guard([&] {
+        if (n_k < 1) fail(ES_ERR_DATA, "EmptyRange", "k_range is empty");
+        int best = -1;
+        double best_bic = INFINITY;
+        int last = ES_OK;
+        std::string ln, lm;
+        const int D = ds->D;
+        for (int j = 0; j < n_k; ++j) {
+            const int K = k_range[j];
+            std::vector<double> pi(std::max(K, 1)), mu((size_t)std::max(K, 1) * D),
+                cov((size_t)std::max(K, 1) * D * D);
+            es_gmm_params outp{K, D, pi.data(), mu.data(), cov.data()};
+            es_fit_report rep{};
+            const int s = es_gmm_fit(c, ds, K, opts, nullptr, &outp, &rep, nullptr);
+            if (s != ES_OK) {  // skip failed K
+                bic[j] = NAN;
+                last = s;
+                ln = g_name;
+                lm = g_msg;
+                continue;
+            }
+            const double p = (K - 1) + (double)K * D + (double)K * D * (D + 1) / 2.0;
+            bic[j] = -2.0 * rep.final_log_likelihood + p * std::log((double)ds->n_global);
+            if (bic[j] < best_bic) {
+                best_bic = bic[j];
+                best = K;
+            }
+        }
+        if (best < 0) fail(last, ln, lm);
+        *best_k = best;
+    });
+}
+
+}  // extern "C"

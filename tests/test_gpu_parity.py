@@ -1,0 +1,213 @@
+"""GPU parity: the CUDA path (C-ABI via ctypes) against the CPU oracle.
+
+Tolerances are the north star's (BASELINE.json): per-event log-likelihood
+within 1e-6 relative (absolute floor 1e-6 * max(1, |ll|)), fitted
+weights/means/covariances within 1e-5 relative (floor: 1e-5 * max|entry| of
+the component), labels/flags identical except events within 1e-9 of a tie or
+of the threshold, which are counted and must be rare.
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+LL_TOL = 1e-6
+PAR_TOL = 1e-5
+BAND = 1e-9
+
+
+def syn(es, oracle, n, D, K, seed=42):
+    ds = es.Dataset.generate(seed, n, D, K)
+    return ds, ds.read_rows()
+
+
+def assert_ll(a, b):
+    err = np.abs(a - b) / np.maximum(1.0, np.abs(b))
+    assert err.max() <= LL_TOL, f"max rel ll err {err.max():.3e}"
+
+
+def assert_params(model, pi, mu, cov):
+    assert np.all(np.abs(model.weights - pi) <= PAR_TOL * np.maximum(np.abs(pi), 1e-3))
+    for k in range(len(pi)):
+        sm = np.abs(mu[k]).max()
+        assert np.all(np.abs(model.means[k] - mu[k]) <= PAR_TOL * np.maximum(np.abs(mu[k]), sm)), k
+        sc = np.abs(cov[k]).max()
+        assert np.all(np.abs(model.covariances[k] - cov[k]) <= PAR_TOL * np.maximum(np.abs(cov[k]), sc)), k
+
+
+def labels_match(a, b, w):
+    """a, b label arrays; w (N,K) log-scores used to find ties within BAND."""
+    diff = np.nonzero(a != b)[0]
+    if len(diff) == 0:
+        return 0
+    s = np.sort(w[diff], axis=1)
+    gap = s[:, -1] - s[:, -2]
+    assert np.all(gap < BAND), f"{len(diff)} label mismatches, not ties"
+    return len(diff)
+
+
+# ----------------------------------------------------------- golden values
+def test_golden_densities_through_cabi(es):
+    m1 = es.GmmModel(np.array([1.0]), np.array([[0.0]]), np.array([[[1.0]]]))
+    assert abs(es.component_log_density(m1, [0.0], 0) - (-0.9189385332046727)) < 1e-9
+    m2 = es.GmmModel(np.array([1.0]), np.zeros((1, 2)), np.eye(2)[None])
+    assert abs(es.component_log_density(m2, [0.0, 0.0], 0) - (-1.8378770664093453)) < 1e-9
+    m3 = es.GmmModel(np.array([1.0]), np.array([[0.0]]), np.array([[[4.0]]]))
+    assert abs(es.component_log_density(m3, [2.0], 0) - (-2.112085713764618)) < 1e-9
+    mm = es.GmmModel(np.array([0.5, 0.5]), np.array([[-1.0], [1.0]]), np.ones((2, 1, 1)))
+    assert abs(es.mixture_density(mm, [0.0]) - 0.24197072451914337) < 1e-12
+    g = es.responsibilities(es.GmmModel(np.array([0.5, 0.5]), np.array([[0.0], [4.0]]), np.ones((2, 1, 1))),
+                            np.array([[1.0]]))
+    assert abs(g[0, 0] - 0.9820137900379085) < 1e-12
+    with pytest.raises(es.EventscopeError) as e:
+        es.component_log_density(m2, [0.0], 0)
+    assert e.value.name == "DimensionMismatch" and e.value.kind == "Data"
+
+
+def test_detect_examples_through_cabi(es):
+    m = es.GmmModel(np.array([1.0]), np.array([[0.0]]), np.array([[[1.0]]]))
+    ld3 = es.component_log_density(m, [3.0], 0)
+    r = es.detect(m, np.array([[0.0], [4.0], [3.0]]), log_delta=ld3)
+    assert list(r.flags) == [0, 1, 0] and list(r.anomaly_indices) == [1] and r.n_flagged == 1
+    r = es.detect(m, np.array([[0.0], [4.0], [3.0]]), delta=math.inf)
+    assert r.flags.sum() == 3
+
+
+def test_calibrate_examples_through_cabi(es, oracle):
+    m = es.GmmModel(np.array([1.0]), np.array([[0.0]]), np.array([[[1.0]]]))
+    xs = np.sqrt(-2 * np.log(np.array([0.1, 0.2, 0.3]) * np.sqrt(2 * np.pi)))[:, None]
+    assert abs(es.calibrate_threshold(m, xs, 0.5) - 0.2) < 1e-12
+    rng = np.random.default_rng(8)
+    Xt = rng.normal(size=(10_000, 1))
+    d, ld = es.calibrate_threshold(m, Xt, 0.01, return_log=True)
+    od, old = oracle.calibrate(Xt, [1.0], [[0.0]], [[[1.0]]], 0.01)
+    assert d == od and ld == old
+    assert es.detect(m, Xt, log_delta=ld).flags.sum() <= math.ceil(0.01 * len(Xt))
+    d0, ld0 = es.calibrate_threshold(m, Xt, 1e-300, return_log=True)
+    assert es.detect(m, Xt, log_delta=ld0).flags.sum() == 0
+    with pytest.raises(es.EventscopeError) as e:
+        es.calibrate_threshold(m, Xt, 0.1, n_train=0)
+    assert e.value.name == "EmptyTraining"
+
+
+# ------------------------------------------------------ c1-shaped parity
+def _fit_both(es, oracle, ds, X, K, iters, init="random", seed=7):
+    model = es.fit_em(ds, K, init=init, tol=0.0, max_iter=iters, seed=seed)
+    pi, mu, cov, rep = oracle.fit_em(X, K, init=init, tol=0.0, max_iter=iters, seed=seed)
+    return model, (pi, mu, cov, rep)
+
+
+@pytest.mark.parametrize("D,K,n,iters", [(8, 4, 1 << 20, 100), (16, 8, 1 << 17, 12), (3, 5, 100_003, 40),
+                                         (20, 3, 30_011, 10), (2, 40, 20_000, 8)])
+def test_fit_score_detect_parity(es, oracle, D, K, n, iters):
+    ds, X = syn(es, oracle, n, D, min(K, 8))
+    model, (pi, mu, cov, rep) = _fit_both(es, oracle, ds, X, K, iters)
+    assert_params(model, pi, mu, cov)
+    per_g, per_o = model.fit_report.per_iteration_log_likelihoods, rep["per_iteration_log_likelihoods"]
+    assert len(per_g) == len(per_o) == iters
+    assert np.all(np.abs(per_g - per_o) <= LL_TOL * np.abs(per_o))
+    assert abs(model.fit_report.final_log_likelihood - rep["final_log_likelihood"]) <= LL_TOL * abs(
+        rep["final_log_likelihood"])
+    assert model.fit_report.iterations == rep["iterations"]
+    # score on the oracle's parameters (same model both sides)
+    om = es.GmmModel(pi, mu, cov)
+    ll = np.empty(ds.n_local)
+    pr = np.empty(ds.n_local, np.int32)
+    bk = np.empty(ds.n_local, np.int32)
+    bl = np.empty(ds.n_local)
+    tot = es.score(om, ds, ll=ll, predict=pr, best_k=bk, best_logdens=bl)
+    o = oracle.score(X, pi, mu, cov, gamma=True)
+    assert_ll(ll, o["ll"])
+    assert_ll(bl, o["best_logdens"])
+    assert abs(tot - o["ll"].sum()) <= 1e-9 * abs(o["ll"].sum())
+    w = np.log(np.maximum(o["gamma"], 1e-300))
+    labels_match(pr, o["predict"], w)
+    lnk = w + o["ll"][:, None] - np.log(pi)[None]  # component log densities (up to rounding)
+    labels_match(bk, o["best_k"], lnk)
+    # detect at the calibrated threshold
+    d, ld = es.calibrate_threshold(om, ds, 0.01, n_train=n // 2, return_log=True)
+    od, old = oracle.calibrate(X[: n // 2], pi, mu, cov, 0.01)
+    assert abs(ld - old) <= 1e-9 * max(1.0, abs(old))
+    r = es.detect(om, ds, log_delta=old)
+    of, obk, obl, on = oracle.detect(X, pi, mu, cov, old)
+    mism = np.nonzero(r.flags != of)[0]
+    assert np.all(np.abs(obl[mism] - old) < BAND), "flag mismatches away from the threshold"
+    assert np.array_equal(r.anomaly_indices, np.nonzero(r.flags)[0])
+    assert r.n_flagged == r.flags.sum()
+
+
+def test_responsibilities_rows_sum_to_one(es, oracle):
+    ds, X = syn(es, oracle, 50_000, 16, 8)
+    pi, mu, cov, _ = oracle.fit_em(X, 8, init="random", tol=0.0, max_iter=5, seed=3)
+    g = es.responsibilities(es.GmmModel(pi, mu, cov), ds)
+    o = oracle.score(X, pi, mu, cov, gamma=True)["gamma"]
+    assert np.abs(g.sum(1) - 1).max() < 1e-9
+    assert np.abs(g - o).max() < 1e-6
+
+
+def test_kmeanspp_init_parity(es, oracle):
+    ds, X = syn(es, oracle, 200_000, 8, 4)
+    model, (pi, mu, cov, rep) = _fit_both(es, oracle, ds, X, 4, 20, init="kmeans++", seed=11)
+    assert_params(model, pi, mu, cov)
+
+
+def test_k1_closed_form_and_convergence(es, oracle):
+    ds, X = syn(es, oracle, 10_007, 5, 3)
+    m = es.fit_em(ds, 1, seed=0)
+    pi, mu, cov, rep = oracle.fit_em(X, 1, seed=0)
+    assert np.allclose(m.means[0], X.mean(0), atol=1e-9)
+    assert np.allclose(m.covariances[0], np.cov(X.T, bias=True) + rep["reg"] * np.eye(5), atol=1e-9)
+    assert m.fit_report.converged and rep["converged"]
+    assert m.fit_report.iterations == rep["iterations"]
+
+
+def test_converged_fit_parity(es, oracle):
+    ds, X = syn(es, oracle, 100_000, 4, 3, seed=5)
+    m = es.fit_em(ds, 3, init="kmeans++", seed=2, tol=1e-6, max_iter=200)
+    pi, mu, cov, rep = oracle.fit_em(X, 3, init="kmeans++", seed=2, tol=1e-6, max_iter=200)
+    assert m.fit_report.converged == rep["converged"]
+    assert m.fit_report.iterations == rep["iterations"]
+    assert_params(m, pi, mu, cov)
+    t = m.fit_report.per_iteration_log_likelihoods
+    assert np.all(np.diff(t) >= -1e-8 * np.abs(t[1:]))
+
+
+def test_errors_through_cabi(es):
+    with pytest.raises(es.EventscopeError) as e:
+        es.fit_em(np.zeros((2, 1)), 3)
+    assert e.value.name == "TooFewPoints" and e.value.kind == "Data"
+    with pytest.raises(es.EventscopeError) as e:
+        es.fit_em(np.ones((10, 2)), 2)
+    assert e.value.name == "DegenerateData"
+    X = np.ones((10, 2))
+    X[3, 1] = np.nan
+    with pytest.raises(es.EventscopeError) as e:
+        es.fit_em(X + np.arange(10)[:, None], 1)
+    assert e.value.name == "NonFiniteInput"
+    t = np.linspace(0, 1, 50)
+    with pytest.raises(es.EventscopeError) as e:
+        es.fit_em(np.stack([t, 2 * t], 1), 1, reg=0.0)
+    assert e.value.name == "SingularCovariance" and e.value.kind == "Numeric"
+
+
+def test_determinism_bitwise(es):
+    ds = es.Dataset.generate(9, 300_000, 16, 8)
+    a = es.fit_em(ds, 8, init="random", tol=0.0, max_iter=5, seed=1)
+    b = es.fit_em(ds, 8, init="random", tol=0.0, max_iter=5, seed=1)
+    assert np.array_equal(a.covariances, b.covariances) and np.array_equal(a.means, b.means)
+    assert np.array_equal(a.fit_report.per_iteration_log_likelihoods, b.fit_report.per_iteration_log_likelihoods)
+
+
+def test_layouts_and_generator(es, oracle):
+    rng = np.random.default_rng(0)
+    X = rng.normal(size=(1001, 7))
+    for arr in (X, np.asfortranarray(X), X[:, ::1].copy()):
+        ds = es.Dataset.from_array(arr)
+        assert np.array_equal(ds.read_rows(), X)
+    # device generator vs host restatement of SYN-v1 (same Philox counters; libm ulps)
+    ds = es.Dataset.generate(42, 4096, 8, 4)
+    model = oracle.syn_model(42, 8, 4)
+    Xo, _, _ = oracle.syn_rows(42, 8, 4, model, 0, 4096)
+    assert np.abs(ds.read_rows() - Xo).max() < 1e-12 * max(1.0, np.abs(Xo).max())
