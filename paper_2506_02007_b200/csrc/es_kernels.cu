@@ -22,7 +22,18 @@
 
 namespace es {
 
-constexpr int kMaxSmem = 227 * 1024;
+// Opt a kernel into the largest dynamic shared memory it can use: the
+// device's per-block opt-in limit minus the kernel's own static __shared__.
+template <class F>
+static void allow_max_smem(F* f) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes a{};
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(f));
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         optin - (int)a.sharedSizeBytes);
+}
 
 namespace {
 
@@ -148,7 +159,7 @@ void launch_rows_to_planar(const double* rows, int64_t n, int D, double* X, int6
     if (n <= 0) return;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_rows_to_planar, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+        allow_max_smem(k_rows_to_planar);
         attr = true;
     }
     const int64_t g = (n + 127) / 128;
@@ -767,7 +778,7 @@ template <int DM, int H>
 static void set_team_attrs(int K) {
     static bool done = false;
     if (!done) {
-        cudaFuncSetAttribute(k_em_team<DM, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+        allow_max_smem(k_em_team<DM, H>);
         done = true;
     }
     (void)K;
@@ -802,8 +813,8 @@ void launch_em_pass(const double* X, int64_t n, int64_t ld, int D, int K, const 
             const size_t smem = (size_t)(D + K) * (T + 1) * sizeof(double);
             static bool attr = false;
             if (!attr) {
-                cudaFuncSetAttribute(k_em_generic<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
-                cudaFuncSetAttribute(k_em_generic<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+                allow_max_smem(k_em_generic<false>);
+                allow_max_smem(k_em_generic<true>);
                 attr = true;
             }
             k_em_generic<false><<<grid, kBlock, smem, s>>>(X, n, ld, D, K, model, model + 3 * K, partial, T);
@@ -821,7 +832,7 @@ void launch_unit_stats(const double* X, int64_t n, int64_t ld, int D, const doub
     const size_t smem = (size_t)(D + 1) * (T + 1) * sizeof(double);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_em_generic<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+        allow_max_smem(k_em_generic<true>);
         attr = true;
     }
     k_em_generic<true><<<grid, kBlock, smem, s>>>(X, n, ld, D, 1, nullptr, center, partial, T);
@@ -839,7 +850,7 @@ static void run_score_team(const double* X, int64_t n, int64_t ld, int D, int K,
                            const ScoreOut& o, double* blocksum, int grid, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_score_team<DM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+        allow_max_smem(k_score_team<DM>);
         attr = true;
     }
     k_score_team<DM><<<grid, kBlock, team_smem<DM, 1>(K, false), s>>>(X, n, ld, D, K, model, o, blocksum);
@@ -1039,7 +1050,7 @@ void launch_finalize(const double* stats, int G, int D, int K, int64_t n_global,
     const size_t smem = (size_t)(stat_k(D) + 5 * D * D + D) * sizeof(double);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+        allow_max_smem(k_finalize);
         attr = true;
     }
     k_finalize<<<K, 128, smem, s>>>(stats, G, D, K, n_global, reg, whitened ? 1 : 0, model, st, record, t);

@@ -42,7 +42,10 @@ struct Fail {
 [[noreturn]] void fail(int code, const std::string& name, const std::string& msg) { throw Fail{code, name, msg}; }
 
 void cu_check(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) fail(ES_ERR_RUNTIME, "CudaError", std::string(what) + ": " + cudaGetErrorString(e));
+    if (e != cudaSuccess) {
+        cudaGetLastError();  // clear the non-sticky last error so later checks do not re-report it
+        fail(ES_ERR_RUNTIME, "CudaError", std::string(what) + ": " + cudaGetErrorString(e));
+    }
 }
 #define CU(x) cu_check((x), #x)
 
@@ -169,7 +172,7 @@ struct es_ctx {
     int num_sms = 148;
     LaunchStats ls;
     DevBuf partial, stats_local, stats_all, model, model_backup, status, scratch, scratch2, scratch3, out_scratch,
-        hist, xbuf, o1, o2, o3, o4, o5;
+        hist, xbuf, o1, o2, o3, o4, o5, kpp;
     IterStatus* h_status = nullptr;  // pinned
     std::vector<double> hbuf;
     // optional CUDA-event timing of the hot kernels (bench.py roofline)
@@ -507,7 +510,7 @@ void em_init_model(es_em_state* st, const es_gmm_params* init, const DataStats& 
             rows.push_back((int64_t)st->rng.below((uint64_t)ds->n_global));
             const int64_t CH = 4096;
             const int64_t nlc = (ds->n_local + CH - 1) / CH;
-            double* d2 = c->scratch3.as<double>(std::max<int64_t>(ds->n_local, 1) + nlc + 8);
+            double* d2 = c->kpp.as<double>(std::max<int64_t>(ds->n_local, 1) + nlc + 8);
             double* parts = d2 + std::max<int64_t>(ds->n_local, 1);
             double* dcen = c->scratch2.as<double>(D);
             std::vector<double> cen;
@@ -815,7 +818,13 @@ int es_dataset_create(es_ctx* c, const double* X, int64_t n_local, int32_t D, in
             if (!X) fail(ES_ERR_DATA, "InvalidInput", "null matrix");
             const bool dev = is_device_ptr(X);
             std::vector<double> packed;
-            if (!(row_stride == D && col_stride == 1) && !(row_stride == 1 && col_stride >= n_local)) {
+            const bool row_major = (row_stride == D && col_stride == 1) || n_local == 1;
+            const bool col_major = !row_major && row_stride == 1 && col_stride >= n_local;
+            if (n_local == 1) {
+                row_stride = D;
+                col_stride = 1;
+            }
+            if (!row_major && !col_major) {
                 if (dev) fail(ES_ERR_DATA, "UnsupportedLayout", "device input must be row- or column-major");
                 packed.resize((size_t)n_local * D);
                 for (int64_t i = 0; i < n_local; ++i)
@@ -824,7 +833,7 @@ int es_dataset_create(es_ctx* c, const double* X, int64_t n_local, int32_t D, in
                 row_stride = D;
                 col_stride = 1;
             }
-            if (row_stride == 1) {
+            if (col_major) {
                 CU(cudaMemcpy2DAsync(ds->X, ds->ld * 8, X, col_stride * 8, n_local * 8, D, cudaMemcpyDefault,
                                      c->stream));
             } else {
