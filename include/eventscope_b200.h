@@ -111,6 +111,10 @@ int es_ctx_destroy(es_ctx* ctx);
 int es_ctx_stream(es_ctx* ctx, void** stream);
 /* Kernel-launch counter (for launch accounting in benchmarks). */
 int es_ctx_launch_count(es_ctx* ctx, int64_t* count);
+/* Arithmetic of the hot kernels: 0 (default) = mixed — FP32 whitening, FP64
+ * statistics / log-likelihoods, FP64 recomputation of every component that
+ * can change an output at the 1e-6 level; 1 = strict FP64 everywhere. */
+int es_ctx_set_precision(es_ctx* ctx, int mode);
 /* CUDA-event timing of the hot kernels on the context stream (resets the
  * accumulators).  which: 0 = fused EM pass, 1 = scoring pass. */
 int es_ctx_set_timing(es_ctx* ctx, int enable);

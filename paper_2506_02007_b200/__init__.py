@@ -162,7 +162,7 @@ class Context:
     exchange callbacks (exchange=(allgather_fn, allreduce_fn))."""
 
     def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
-                 exchange=None):
+                 exchange=None, precision: str = "mixed"):
         lib = load_library()
         self._lib = lib
         h = C.c_void_p()
@@ -179,6 +179,12 @@ class Context:
             _check(lib.es_ctx_create(device, C.byref(h)))
         self.handle = h
         self.device, self.rank, self.world = device, rank, world
+        self.set_precision(os.environ.get("ES_PRECISION", precision))
+
+    def set_precision(self, mode: str) -> None:
+        """'mixed' (default: FP32 whitening, FP64 statistics) or 'fp64' (strict)."""
+        _check(self._lib.es_ctx_set_precision(self.handle, {"mixed": 0, "fp64": 1}[mode]))
+        self.precision = mode
 
     @staticmethod
     def nccl_unique_id() -> bytes:

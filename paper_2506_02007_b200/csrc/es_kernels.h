@@ -71,6 +71,20 @@ void launch_planar_to_rows(const double* X, int64_t ld, int D, int64_t row0, int
 // parts[chunk] = fixed-order sum of d2 over 4096-row chunks.
 void launch_kpp_update(const double* X, int64_t n, int64_t ld, int D, const double* center, double* d2,
                        double* parts, bool first, cudaStream_t s, LaunchStats& ls);
+// Mixed-precision fast path (es_fast.cu): FP32 whitening, FP64 statistics.
+// `center` (D doubles) is subtracted in FP64 before the FP32 conversion.
+bool em_fast_supported(int D, int K);
+void launch_em_fast(const double* X, int64_t n, int64_t ld, int D, int K, const double* model, const double* center,
+                    double* partial, int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
+// tcgen05 E-step variant of the fused pass (D <= 16, K <= 8); ES_EM_KERNEL=simt
+// selects the SIMT FP32 kernel instead.
+bool em_tc_enabled();
+void launch_em_tc(const double* X, int64_t n, int64_t ld, int D, int K, const double* model, const double* center,
+                  double* partial, int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
+bool score_fast_supported(int D, int K, const ScoreOut& o);
+void launch_score_fast(const double* X, int64_t n, int64_t ld, int D, int K, const double* model,
+                       const double* center, const ScoreOut& o, double* blocksum, int num_sms, int* nblk,
+                       cudaStream_t s, LaunchStats& ls);
 // SYN-v1 rows [grow0, grow0+n) written into planar X (local row = global - grow0).
 void launch_synth(double* X, int64_t ld, int64_t n, int64_t grow0, int D, int K, const double* syn_model,
                   uint64_t seed, cudaStream_t s, LaunchStats& ls);

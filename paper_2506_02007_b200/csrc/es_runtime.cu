@@ -172,7 +172,8 @@ struct es_ctx {
     int num_sms = 148;
     LaunchStats ls;
     DevBuf partial, stats_local, stats_all, model, model_backup, status, scratch, scratch2, scratch3, out_scratch,
-        hist, xbuf, o1, o2, o3, o4, o5, kpp;
+        hist, xbuf, o1, o2, o3, o4, o5, kpp, center;
+    int precision = 0;  // 0 = mixed (FP32 whitening, FP64 statistics), 1 = strict FP64
     IterStatus* h_status = nullptr;  // pinned
     std::vector<double> hbuf;
     // optional CUDA-event timing of the hot kernels (bench.py roofline)
@@ -267,6 +268,8 @@ struct es_em_state {
     es_fit_opts opts{};
     double reg = 0.0;
     std::vector<double> S;  // data covariance (D x D)
+    std::vector<double> mean;  // data mean: FP64 centre of the mixed-precision path
+    DevBuf dcenter;
     SplitMix64 rng{0};
     std::vector<double> per_iter;
     int t = 0;          // E-steps done
@@ -416,6 +419,14 @@ double* model_for(es_ctx* c, const es_gmm_params* p, int D) {
     check_params(p, D);
     double* m = c->model.as<double>(mstride(p->K, D));
     upload_model(c, m, p->K, D, p->weights, p->means, p->covariances);
+    // FP64 centre for the mixed-precision scorer: the model's mean sum_k pi_k mu_k
+    std::vector<double> cen(D, 0.0);
+    double z = 0.0;
+    for (int k = 0; k < p->K; ++k) z += p->weights[k];
+    for (int k = 0; k < p->K; ++k)
+        for (int j = 0; j < D; ++j) cen[j] += (z > 0 ? p->weights[k] / z : 1.0 / p->K) * p->means[(size_t)k * D + j];
+    double* dc = c->center.as<double>(D);
+    CU(cudaMemcpyAsync(dc, cen.data(), D * 8, cudaMemcpyHostToDevice, c->stream));
     return m;
 }
 
@@ -436,14 +447,25 @@ struct Out {
     }
 };
 
-double run_score(es_ctx* c, es_dataset* ds, const double* dmodel, int K, ScoreOut o) {
+// Scoring launch: mixed-precision kernel when supported, FP64 team kernel otherwise.
+void score_launch(es_ctx* c, const double* X, int64_t n, int64_t ld, int D, int K, const double* dmodel,
+                  const double* center, const ScoreOut& o, double* bs, int* nblk) {
+    if (c->precision == 0 && center && score_fast_supported(D, K, o))
+        launch_score_fast(X, n, ld, D, K, dmodel, center, o, bs, c->num_sms, nblk, c->stream, c->ls);
+    else
+        launch_score(X, n, ld, D, K, dmodel, o, bs, c->num_sms, nblk, c->stream, c->ls);
+}
+
+size_t score_blocks(es_ctx* c, int D, int K) { return (size_t)2 * std::max(score_grid(D, K, c->num_sms), 2 * c->num_sms) + 2; }
+
+double run_score(es_ctx* c, es_dataset* ds, const double* dmodel, int K, ScoreOut o, const double* center) {
     const int D = ds->D;
-    double* bs = c->scratch.as<double>((size_t)2 * score_grid(D, K, c->num_sms) + 2);
+    double* bs = c->scratch.as<double>(score_blocks(c, D, K));
     double loc = 0.0;
     if (ds->n_local > 0) {
         int nblk = 0;
         c->t_begin();
-        launch_score(ds->X, ds->n_local, ds->ld, D, K, dmodel, o, bs, c->num_sms, &nblk, c->stream, c->ls);
+        score_launch(c, ds->X, ds->n_local, ds->ld, D, K, dmodel, center, o, bs, &nblk);
         c->t_end(c->score_ms, c->score_launches);
         double* red = c->scratch2.as<double>(2);
         launch_reduce_blocks(bs, nblk, 2, red, c->stream, c->ls);
@@ -598,6 +620,8 @@ void em_begin(es_em_state* st, const es_gmm_params* init) {
         if (deg) fail(ES_ERR_DATA, "DegenerateData", "all points identical and K > 1");
     }
     st->S = dsx.S;
+    st->mean = dsx.mean;
+    CU(cudaMemcpyAsync(st->dcenter.as<double>(D), dsx.mean.data(), D * 8, cudaMemcpyHostToDevice, c->stream));
     st->reg = st->opts.reg < 0 ? default_reg(dsx.S, D) : st->opts.reg;
     st->rng = SplitMix64(st->opts.seed);
     em_init_model(st, init, dsx);
@@ -616,14 +640,25 @@ bool em_iterate(es_em_state* st) {
     bool whitened = true;
     if (ds->n_local > 0) {
         int nblk = 0;
-        double* part = c->partial.as<double>((size_t)em_grid(D, K, c->num_sms) * NE1);
+        double* part = c->partial.as<double>((size_t)std::max(em_grid(D, K, c->num_sms), c->num_sms) * NE1);
         c->t_begin();
-        launch_em_pass(ds->X, ds->n_local, ds->ld, D, K, dmodel, part, c->num_sms, &nblk, &whitened, c->stream, c->ls);
+        if (c->precision == 0 && em_fast_supported(D, K)) {
+            if (em_tc_enabled())
+                launch_em_tc(ds->X, ds->n_local, ds->ld, D, K, dmodel, st->dcenter.as<double>(D), part, c->num_sms,
+                             &nblk, c->stream, c->ls);
+            else
+                launch_em_fast(ds->X, ds->n_local, ds->ld, D, K, dmodel, st->dcenter.as<double>(D), part,
+                               c->num_sms, &nblk, c->stream, c->ls);
+            whitened = false;
+        } else {
+            launch_em_pass(ds->X, ds->n_local, ds->ld, D, K, dmodel, part, c->num_sms, &nblk, &whitened, c->stream,
+                           c->ls);
+        }
         c->t_end(c->em_ms, c->em_launches);
         launch_reduce_blocks(part, nblk, NE1, loc, c->stream, c->ls);
     } else {
         CU(cudaMemsetAsync(loc, 0, NE1 * 8, c->stream));
-        whitened = em_path(D, K) != EmPath::Generic;
+        whitened = !(c->precision == 0 && em_fast_supported(D, K)) && em_path(D, K) != EmPath::Generic;
     }
     double* all = c->stats_all.as<double>((size_t)NE1 * c->world);
     c->allgather(loc, all, NE1);
@@ -767,6 +802,13 @@ int es_ctx_stream(es_ctx* c, void** stream) {
 
 int es_ctx_launch_count(es_ctx* c, int64_t* count) {
     return guard([&] { *count = c->ls.launches; });
+}
+
+int es_ctx_set_precision(es_ctx* c, int mode) {
+    return guard([&] {
+        if (mode != 0 && mode != 1) fail(ES_ERR_DATA, "RangeViolation", "precision mode must be 0 or 1");
+        c->precision = mode;
+    });
 }
 
 int es_ctx_set_timing(es_ctx* c, int enable) {
@@ -989,7 +1031,7 @@ int es_gmm_em_end(es_em_state* st, es_gmm_params* out, es_fit_report* rep, doubl
         const int K = st->K, D = st->D;
         double* dmodel = c->model.as<double>(mstride(K, D));
         double final_ll = st->last;
-        if (!st->converged) final_ll = run_score(c, st->ds, dmodel, K, ScoreOut{});
+        if (!st->converged) final_ll = run_score(c, st->ds, dmodel, K, ScoreOut{}, st->dcenter.as<double>(D));
         if (out) {
             if (out->K != K || out->D != D) fail(ES_ERR_DATA, "DimensionMismatch", "output params shape");
             ModelView mv{K, D, dmodel};
@@ -1041,7 +1083,7 @@ int es_gmm_score(es_ctx* c, es_dataset* ds, const es_gmm_params* p, double* ll, 
         o.best_ld = o_bl.dev;
         o.predict = o_pr.dev;
         o.best_k = o_bk.dev;
-        const double tot = run_score(c, ds, m, p->K, o);
+        const double tot = run_score(c, ds, m, p->K, o, c->center.as<double>(ds->D));
         o_ll.finish(c->stream);
         o_bl.finish(c->stream);
         o_pr.finish(c->stream);
@@ -1058,7 +1100,7 @@ int es_gmm_responsibilities(es_ctx* c, es_dataset* ds, const es_gmm_params* p, d
         Out<double> o_g(gamma, (size_t)ds->n_local * p->K, c->o1);
         ScoreOut o;
         o.gamma = o_g.dev;
-        run_score(c, ds, m, p->K, o);
+        run_score(c, ds, m, p->K, o, c->center.as<double>(ds->D));
         o_g.finish(c->stream);
         c->sync();
     });
@@ -1123,7 +1165,7 @@ int es_gmm_detect(es_ctx* c, es_dataset* ds, const es_gmm_params* p, double log_
         o.best_ld = o_bl.dev;
         o.log_delta = log_delta;
         o.mode = mode;
-        run_score(c, ds, m, p->K, o);
+        run_score(c, ds, m, p->K, o, c->center.as<double>(ds->D));
         int64_t* cnt = c->scratch2.as<int64_t>((n + 4095) / 4096 + 2);
         int64_t* dcount = cnt + (n + 4095) / 4096 + 1;
         launch_compact(dflags, n, ds->row_offset, cnt, o_idx.dev, dcount, c->stream, c->ls);
@@ -1161,8 +1203,8 @@ int es_gmm_calibrate(es_ctx* c, es_dataset* ds, const es_gmm_params* p, int64_t 
             if (mode == 1) o.ll = keys;
             else o.best_ld = keys;
             int nblk = 0;
-            double* bs = c->scratch.as<double>((size_t)2 * score_grid(ds->D, p->K, c->num_sms) + 2);
-            launch_score(ds->X, nloc, ds->ld, ds->D, p->K, m, o, bs, c->num_sms, &nblk, c->stream, c->ls);
+            double* bs = c->scratch.as<double>(score_blocks(c, ds->D, p->K));
+            score_launch(c, ds->X, nloc, ds->ld, ds->D, p->K, m, c->center.as<double>(ds->D), o, bs, &nblk);
             c->check_launch();
         }
         // q-quantile, linear interpolation between order statistics, h = (n-1) q

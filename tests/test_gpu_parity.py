@@ -18,6 +18,15 @@ PAR_TOL = 1e-5
 BAND = 1e-9
 
 
+@pytest.fixture(params=["mixed", "fp64"])
+def prec(request, es):
+    """Both arithmetic modes of the product path."""
+    ctx = es.default_context()
+    ctx.set_precision(request.param)
+    yield request.param
+    ctx.set_precision("mixed")
+
+
 def syn(es, oracle, n, D, K, seed=42):
     ds = es.Dataset.generate(seed, n, D, K)
     return ds, ds.read_rows()
@@ -101,7 +110,7 @@ def _fit_both(es, oracle, ds, X, K, iters, init="random", seed=7):
 
 @pytest.mark.parametrize("D,K,n,iters", [(8, 4, 1 << 20, 100), (16, 8, 1 << 17, 12), (3, 5, 100_003, 40),
                                          (20, 3, 30_011, 10), (2, 40, 20_000, 8)])
-def test_fit_score_detect_parity(es, oracle, D, K, n, iters):
+def test_fit_score_detect_parity(es, oracle, prec, D, K, n, iters):
     ds, X = syn(es, oracle, n, D, min(K, 8))
     model, (pi, mu, cov, rep) = _fit_both(es, oracle, ds, X, K, iters)
     assert_params(model, pi, mu, cov)
@@ -138,7 +147,7 @@ def test_fit_score_detect_parity(es, oracle, D, K, n, iters):
     assert r.n_flagged == r.flags.sum()
 
 
-def test_responsibilities_rows_sum_to_one(es, oracle):
+def test_responsibilities_rows_sum_to_one(es, oracle, prec):
     ds, X = syn(es, oracle, 50_000, 16, 8)
     pi, mu, cov, _ = oracle.fit_em(X, 8, init="random", tol=0.0, max_iter=5, seed=3)
     g = es.responsibilities(es.GmmModel(pi, mu, cov), ds)
@@ -147,7 +156,7 @@ def test_responsibilities_rows_sum_to_one(es, oracle):
     assert np.abs(g - o).max() < 1e-6
 
 
-def test_kmeanspp_init_parity(es, oracle):
+def test_kmeanspp_init_parity(es, oracle, prec):
     ds, X = syn(es, oracle, 200_000, 8, 4)
     model, (pi, mu, cov, rep) = _fit_both(es, oracle, ds, X, 4, 20, init="kmeans++", seed=11)
     assert_params(model, pi, mu, cov)
@@ -163,7 +172,7 @@ def test_k1_closed_form_and_convergence(es, oracle):
     assert m.fit_report.iterations == rep["iterations"]
 
 
-def test_converged_fit_parity(es, oracle):
+def test_converged_fit_parity(es, oracle, prec):
     ds, X = syn(es, oracle, 100_000, 4, 3, seed=5)
     m = es.fit_em(ds, 3, init="kmeans++", seed=2, tol=1e-6, max_iter=200)
     pi, mu, cov, rep = oracle.fit_em(X, 3, init="kmeans++", seed=2, tol=1e-6, max_iter=200)
@@ -192,7 +201,7 @@ def test_errors_through_cabi(es):
     assert e.value.name == "SingularCovariance" and e.value.kind == "Numeric"
 
 
-def test_determinism_bitwise(es):
+def test_determinism_bitwise(es, prec):
     ds = es.Dataset.generate(9, 300_000, 16, 8)
     a = es.fit_em(ds, 8, init="random", tol=0.0, max_iter=5, seed=1)
     b = es.fit_em(ds, 8, init="random", tol=0.0, max_iter=5, seed=1)
