@@ -379,18 +379,46 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
 
 }  // namespace
 
+// packed FP32 pair helpers (sm_100a FFMA2)
+__device__ __forceinline__ uint64_t pack2(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void unpack2(uint64_t v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ void ffma2(uint64_t& acc, uint64_t a, uint64_t b) {
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+// Gram accumulator layout for DM = 16 in FP32 pairs: row a covers b >= a as
+// (odd a: one single (a,a)) + pairs (2m, 2m+1) for 2m >= a.
+struct GramPairs {
+    static constexpr int NP = 64;   // pairs
+    static constexpr int NSG = 8;   // singles (odd diagonal entries)
+};
+
 __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, int64_t n, int64_t ld, int D, int K,
                                                   const double* __restrict__ model,
                                                   const double* __restrict__ center, double* __restrict__ partial) {
     constexpr int DM = 16;
     using C = FastCfg<DM>;
     extern __shared__ __align__(1024) unsigned char smraw[];
-    // tensor-core operands first (16-byte aligned core matrices)
     unsigned char* sAh = smraw;                         // 2 sub-tiles x 12 KB
     unsigned char* sAl = sAh + 2 * kOpBytes;            // 2 x 12 KB
     unsigned char* sBh = sAl + 2 * kOpBytes;            // 12 KB
     unsigned char* sBl = sBh + kOpBytes;                // 12 KB
-    float* sMu = reinterpret_cast<float*>(sBl + kOpBytes);  // 8*DM
+    double* sXd = reinterpret_cast<double*>(sBl + kOpBytes);  // 2 buffers x DM x T FP64 (bulk-prefetched tiles)
+    float* sMu = reinterpret_cast<float*>(sXd + 2 * DM * kT);  // 8*DM
     float* sCst = sMu + kKmax * DM;                     // 8
     float* sX = sCst + kKmax;                           // DM*XS
     float* lstG = sX + DM * C::XS;                      // 8*T
@@ -401,12 +429,11 @@ __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, i
     double* sAcc = reinterpret_cast<double*>(tot + 8);
     double* sRed = sAcc + kKmax * C::NS;
     double* sC = sRed + kT;
-    __shared__ uint64_t mbar;
+    __shared__ uint64_t mbar_mma, mbar_x[2];
     __shared__ uint32_t tmem_slot;
 
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     ModelView mv{K, D, const_cast<double*>(model)};
-    // ---- one-time staging: B = [W | -W mu'] split hi/lo, mu', constants
     for (int j = t; j < DM; j += kT) sC[j] = j < D ? center[j] : 0.0;
     __syncthreads();
     for (int e = t; e < kTileRows * kKA; e += kT) {
@@ -433,67 +460,120 @@ __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, i
     }
     for (int k = t; k < kKmax; k += kT) sCst[k] = k < K ? (float)(mv.logpi()[k] + mv.lognorm()[k]) : -INFINITY;
     for (int e = t; e < kKmax * C::NS; e += kT) sAcc[e] = 0.0;
-    // constant feature columns of A (feature 16 = 1, 17..23 = 0) never change
     for (int e = t; e < 2 * kTileRows * (kKA - DM); e += kT) {
-        const int s = e / (kTileRows * (kKA - DM)), rr = e % (kTileRows * (kKA - DM));
+        const int s2 = e / (kTileRows * (kKA - DM)), rr = e % (kTileRows * (kKA - DM));
         const int row = rr / (kKA - DM), kk = DM + rr % (kKA - DM);
-        const uint32_t one = kk == DM ? 0x3F800000u : 0u;
-        *reinterpret_cast<uint32_t*>(sAh + s * kOpBytes + op_off(row, kk)) = one;
-        *reinterpret_cast<uint32_t*>(sAl + s * kOpBytes + op_off(row, kk)) = 0u;
+        *reinterpret_cast<uint32_t*>(sAh + s2 * kOpBytes + op_off(row, kk)) = kk == DM ? 0x3F800000u : 0u;
+        *reinterpret_cast<uint32_t*>(sAl + s2 * kOpBytes + op_off(row, kk)) = 0u;
     }
+    // planes beyond D stay zero in both prefetch buffers
+    for (int e = t; e < 2 * DM * kT; e += kT) sXd[e] = 0.0;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(&tmem_slot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (t == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mbar)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mbar_mma)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mbar_x[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mbar_x[1])));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_slot;
-    const uint32_t bar = su32(&mbar);
-    uint32_t phase = 0;
+    const uint32_t bar = su32(&mbar_mma);
+    uint32_t phase = 0, xphase[2] = {0, 0};
     const uint64_t dBh = umma_desc(su32(sBh)), dBl = umma_desc(su32(sBl));
+    const int64_t ntiles = (n + kT - 1) / kT;
+    // full tiles are prefetched with bulk async copies; the tail tile is loaded directly
+    auto prefetch = [&](int64_t tile, int buf) {
+        if (tile >= ntiles || (tile + 1) * kT > n) return;
+        const uint32_t b = su32(&mbar_x[buf]);
+        mbar_expect_tx(b, (uint32_t)(D * kT * 8));
+        for (int j = 0; j < D; ++j)
+            bulk_g2s(su32(sXd + (buf * DM + j) * kT), X + (int64_t)j * ld + tile * kT, kT * 8, b);
+    };
+    if (t == 0) prefetch(blockIdx.x, 0);
 
     const int kw = warp;
     const bool mact = kw < K;
-    float acc[C::NS];
+    uint64_t accp[GramPairs::NP];
+    float accs[GramPairs::NSG];
+    uint64_t acc1[DM / 2];
+    float accn = 0.f;
 #pragma unroll
-    for (int j = 0; j < C::NS; ++j) acc[j] = 0.f;
+    for (int j = 0; j < GramPairs::NP; ++j) accp[j] = 0;
+#pragma unroll
+    for (int j = 0; j < GramPairs::NSG; ++j) accs[j] = 0.f;
+#pragma unroll
+    for (int j = 0; j < DM / 2; ++j) acc1[j] = 0;
     int since_flush = 0;
     double ll_acc = 0.0;
     const unsigned lt_mask = (1u << lane) - 1u;
+    // flush: warp butterfly of each FP32 accumulator, lane (idx % 32) adds it to the FP64 shared total
+    auto flush1 = [&](float v, int idx) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((idx & 31) == lane) sAcc[kw * C::NS + idx] += (double)v;
+    };
     auto flush = [&]() {
         if (!mact) return;
+        flush1(accn, 0);
+        accn = 0.f;
 #pragma unroll
-        for (int j = 0; j < C::NS; ++j) {
-            float v = acc[j];
+        for (int m = 0; m < DM / 2; ++m) {
+            float lo, hi;
+            unpack2(acc1[m], lo, hi);
+            flush1(lo, 1 + 2 * m);
+            flush1(hi, 2 + 2 * m);
+            acc1[m] = 0;
+        }
+        int ip = 0, is = 0;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if ((j & 31) == lane) sAcc[kw * C::NS + j] += (double)v;
-            acc[j] = 0.f;
+        for (int a = 0; a < DM; ++a) {
+            const int base = 1 + DM + a * DM - (a * (a - 1)) / 2;  // packed index of (a, a)
+            if (a & 1) {
+                flush1(accs[is], base);
+                accs[is++] = 0.f;
+            }
+#pragma unroll
+            for (int m = (a + 1) / 2; m < DM / 2; ++m) {
+                float lo, hi;
+                unpack2(accp[ip], lo, hi);
+                flush1(lo, base + (2 * m - a));
+                flush1(hi, base + (2 * m + 1 - a));
+                accp[ip++] = 0;
+            }
         }
     };
     const int sub = t >> 7, row = t & 127;
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    int buf = 0;
 
-    for (int64_t tile = blockIdx.x;; tile += gridDim.x) {
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t t0 = tile * kT;
-        if (t0 >= n) break;
         const int64_t i = t0 + t;
         const bool valid = i < n;
-        // ---------------- operand A: x' = x - c (FP64) -> FP32 -> TF32 hi/lo
+        const bool full = t0 + kT <= n;
+        if (full) {
+            mbar_wait(su32(&mbar_x[buf]), xphase[buf]);
+            xphase[buf] ^= 1;
+        }
+        // ---------------- operand A from the prefetched FP64 tile
         unsigned char* ah = sAh + sub * kOpBytes;
         unsigned char* al = sAl + sub * kOpBytes;
+        const double* xs = sXd + buf * DM * kT;
 #pragma unroll
         for (int j = 0; j < DM; j += 4) {
             float f[4];
             uint32_t h[4], l[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                f[q] = (valid && j + q < D) ? (float)(__ldg(X + (int64_t)(j + q) * ld + i) - sC[j + q]) : 0.f;
+                double xv;
+                if (full) xv = xs[(j + q) * kT + t];
+                else xv = (valid && j + q < D) ? __ldg(X + (int64_t)(j + q) * ld + i) : 0.0;
+                f[q] = (valid && j + q < D) ? (float)(xv - sC[j + q]) : 0.f;
                 sX[(j + q) * C::XS + t] = f[q];
                 h[q] = tf32(f[q]);
                 l[q] = tf32(f[q] - __uint_as_float(h[q]));
@@ -504,8 +584,8 @@ __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, i
         proxy_fence();
         tc_fence_before();
         __syncthreads();
-        // ---------------- 2 sub-tiles x (3 terms x 3 K-steps) UMMAs, one issuing thread
         if (t == 0) {
+            prefetch(tile + gridDim.x, buf ^ 1);  // buffer buf^1 was consumed one tile ago
             tc_fence_after();
 #pragma unroll
             for (int s2 = 0; s2 < 2; ++s2) {
@@ -513,7 +593,7 @@ __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, i
                 const uint64_t dAh = umma_desc(su32(sAh + s2 * kOpBytes)), dAl = umma_desc(su32(sAl + s2 * kOpBytes));
 #pragma unroll
                 for (int ks = 0; ks < kKA / 8; ++ks) {
-                    const uint64_t ko = (uint64_t)((2 * ks * kLBO) >> 4);  // advance start address by 2 K chunks
+                    const uint64_t ko = (uint64_t)((2 * ks * kLBO) >> 4);
                     mma_tf32(d, dAh + ko, dBh + ko, ks > 0 ? 1u : 0u);
                     mma_tf32(d, dAh + ko, dBl + ko, 1u);
                     mma_tf32(d, dAl + ko, dBh + ko, 1u);
@@ -522,10 +602,11 @@ __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, i
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                          : "memory");
         }
+        buf ^= 1;
         mbar_wait(bar, phase);
         phase ^= 1;
         tc_fence_after();
-        // ---------------- epilogue: thread per event, all components from its TMEM row
+        // ---------------- epilogue
         float w[kKmax];
         float m = -INFINITY;
 #pragma unroll
@@ -533,10 +614,15 @@ __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, i
             float u[16];
             tmem_ld16(tmem + lane_base + 128 * sub + 16 * k, u);
             tmem_wait_ld();
-            float q = 0.f;
+            uint64_t q2 = 0;
 #pragma unroll
-            for (int r = 0; r < 16; ++r) q = fmaf(u[r], u[r], q);
-            w[k] = sCst[k] - 0.5f * q;
+            for (int r = 0; r < 16; r += 2) {
+                const uint64_t uu = pack2(u[r], u[r + 1]);
+                ffma2(q2, uu, uu);
+            }
+            float qa, qb;
+            unpack2(q2, qa, qb);
+            w[k] = sCst[k] - 0.5f * (qa + qb);
             m = fmaxf(m, w[k]);
         }
         tc_fence_before();
@@ -557,12 +643,12 @@ __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, i
         }
         __syncthreads();
         if (t < kKmax) {
-            int a = 0;
+            int a2 = 0;
             for (int wv = 0; wv < 8; ++wv) {
-                off[wv * 8 + t] = a;
-                a += cnt[wv * 8 + t];
+                off[wv * 8 + t] = a2;
+                a2 += cnt[wv * 8 + t];
             }
-            tot[t] = a;
+            tot[t] = a2;
         }
         __syncthreads();
 #pragma unroll
@@ -573,7 +659,7 @@ __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, i
                 lstG[k * kT + p] = g[k];
             }
         __syncthreads();
-        // ---------------- M-phase (as k_em_fast)
+        // ---------------- M-phase: packed FP32 pairs
         if (mact) {
             const int nk = tot[kw];
             const float* muk = sMu + kw * DM;
@@ -584,20 +670,30 @@ __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, i
                 const float gg = ve ? lstG[kw * kT + e] : 0.f;
                 float d[DM];
 #pragma unroll
-                for (int a = 0; a < DM; ++a) d[a] = sX[a * C::XS + tt] - muk[a];
-                acc[0] += gg;
-                int p = 1 + DM;
+                for (int a2 = 0; a2 < DM; ++a2) d[a2] = sX[a2 * C::XS + tt] - muk[a2];
+                uint64_t d2[DM / 2];
 #pragma unroll
-                for (int a = 0; a < DM; ++a) {
-                    const float ga = gg * d[a];
-                    acc[1 + a] += ga;
+                for (int mm = 0; mm < DM / 2; ++mm) d2[mm] = pack2(d[2 * mm], d[2 * mm + 1]);
+                accn += gg;
+                const uint64_t g2 = pack2(gg, gg);
 #pragma unroll
-                    for (int b = a; b < DM; ++b) {
-                        acc[p] = fmaf(ga, d[b], acc[p]);
-                        ++p;
+                for (int mm = 0; mm < DM / 2; ++mm) ffma2(acc1[mm], g2, d2[mm]);
+                int ip = 0, is = 0;
+#pragma unroll
+                for (int a2 = 0; a2 < DM; ++a2) {
+                    const float ga = gg * d[a2];
+                    const uint64_t ga2 = pack2(ga, ga);
+                    if (a2 & 1) {
+                        accs[is] = fmaf(ga, d[a2], accs[is]);
+                        ++is;
+                    }
+#pragma unroll
+                    for (int mm = (a2 + 1) / 2; mm < DM / 2; ++mm) {
+                        ffma2(accp[ip], ga2, d2[mm]);
+                        ++ip;
                     }
                 }
-                if (++since_flush == 32) {
+                if (++since_flush == 128) {
                     flush();
                     since_flush = 0;
                 }
@@ -615,13 +711,13 @@ __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, i
         if (r <= D) {
             j = r;
         } else {
-            int p = r - 1 - D, a = 0;
-            while (p >= D - a) {
-                p -= D - a;
-                ++a;
+            int p = r - 1 - D, a2 = 0;
+            while (p >= D - a2) {
+                p -= D - a2;
+                ++a2;
             }
-            const int b = a + p;
-            j = 1 + DM + (a * DM - (a * (a - 1)) / 2 + (b - a));
+            const int b2 = a2 + p;
+            j = 1 + DM + (a2 * DM - (a2 * (a2 - 1)) / 2 + (b2 - a2));
         }
         myp[e] = sAcc[k * C::NS + j];
     }
@@ -633,7 +729,7 @@ __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, i
 
 static size_t em_tc_smem() {
     using C = FastCfg<16>;
-    size_t b = (size_t)6 * kOpBytes;
+    size_t b = (size_t)6 * kOpBytes + (size_t)2 * 16 * kT * 8;
     b += (size_t)(kKmax * 16 + kKmax + 16 * C::XS + kKmax * kT) * 4;
     b += (size_t)kKmax * kT * 2;
     b += (64 + 64 + 8) * 4;
