@@ -355,7 +355,8 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
           "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
+        : "r"(taddr)
+        : "memory");
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
 }
@@ -407,6 +408,23 @@ struct GramPairs {
     static constexpr int NSG = 8;   // singles (odd diagonal entries)
 };
 
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
+constexpr int kXR = 20;  // row-major FP32 x' stride (16 + 4 pad floats = 80 B)
+
+// Software pipeline per CTA (one tile = 256 events = 2 UMMA M-tiles):
+//   [wait MMA(j)] [epilogue(j): TMEM -> w, LSE, gamma lists] [A-prep(j+1) from
+//   the bulk-prefetched X tile] [issue MMA(j+1), prefetch X(j+2)] [M-phase(j)]
+// so the tensor cores and the copy engine work under the FP32 M-phase.
 __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, int64_t n, int64_t ld, int D, int K,
                                                   const double* __restrict__ model,
                                                   const double* __restrict__ center, double* __restrict__ partial) {
@@ -417,14 +435,16 @@ __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, i
     unsigned char* sAl = sAh + 2 * kOpBytes;            // 2 x 12 KB
     unsigned char* sBh = sAl + 2 * kOpBytes;            // 12 KB
     unsigned char* sBl = sBh + kOpBytes;                // 12 KB
-    double* sXd = reinterpret_cast<double*>(sBl + kOpBytes);  // 2 buffers x DM x T FP64 (bulk-prefetched tiles)
-    float* sMu = reinterpret_cast<float*>(sXd + 2 * DM * kT);  // 8*DM
-    float* sCst = sMu + kKmax * DM;                     // 8
-    float* sX = sCst + kKmax;                           // DM*XS
-    float* lstG = sX + DM * C::XS;                      // 8*T
-    uint16_t* lstT = reinterpret_cast<uint16_t*>(lstG + kKmax * kT);
-    int* cnt = reinterpret_cast<int*>(lstT + kKmax * kT);
-    int* off = cnt + 64;
+    double* sXd = reinterpret_cast<double*>(sBl + kOpBytes);   // 2 x DM x T FP64 (bulk-prefetched tiles)
+    float* sXr = reinterpret_cast<float*>(sXd + 2 * DM * kT);  // 2 x T x kXR FP32 rows (x' - for the M-phase)
+    float* sNMu = sXr + 2 * kT * kXR;                   // 8 x DM: -mu'
+    float* sCst = sNMu + kKmax * DM;                    // 8
+    float* sThr = sCst + kKmax;                         // 8 pruning thresholds
+    float* lstG = sThr + kKmax;                         // 8*T
+    float* sG = lstG + kKmax * kT;                      // 8*T responsibilities of the tile
+    uint16_t* lstT = reinterpret_cast<uint16_t*>(sG + kKmax * kT);
+    unsigned* bal = reinterpret_cast<unsigned*>(lstT + kKmax * kT);  // 8 warps x 8 comps ballots
+    int* off = reinterpret_cast<int*>(bal + 64);
     int* tot = off + 64;
     double* sAcc = reinterpret_cast<double*>(tot + 8);
     double* sRed = sAcc + kKmax * C::NS;
@@ -456,9 +476,13 @@ __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, i
     }
     for (int e = t; e < kKmax * DM; e += kT) {
         const int k = e / DM, j = e % DM;
-        sMu[e] = (k < K && j < D) ? (float)(mv.mu()[k * D + j] - sC[j]) : 0.f;
+        sNMu[e] = (k < K && j < D) ? -(float)(mv.mu()[k * D + j] - sC[j]) : 0.f;
     }
-    for (int k = t; k < kKmax; k += kT) sCst[k] = k < K ? (float)(mv.logpi()[k] + mv.lognorm()[k]) : -INFINITY;
+    for (int k = t; k < kKmax; k += kT) {
+        sCst[k] = k < K ? (float)(mv.logpi()[k] + mv.lognorm()[k]) : -INFINITY;
+        // certified pruning: skipped responsibility mass <= N * 1e-9 * pi_k = 1e-9 N_k
+        sThr[k] = k < K ? fmaxf((float)(1e-9 * mv.pi()[k]), 1e-30f) : INFINITY;
+    }
     for (int e = t; e < kKmax * C::NS; e += kT) sAcc[e] = 0.0;
     for (int e = t; e < 2 * kTileRows * (kKA - DM); e += kT) {
         const int s2 = e / (kTileRows * (kKA - DM)), rr = e % (kTileRows * (kKA - DM));
@@ -466,7 +490,6 @@ __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, i
         *reinterpret_cast<uint32_t*>(sAh + s2 * kOpBytes + op_off(row, kk)) = kk == DM ? 0x3F800000u : 0u;
         *reinterpret_cast<uint32_t*>(sAl + s2 * kOpBytes + op_off(row, kk)) = 0u;
     }
-    // planes beyond D stay zero in both prefetch buffers
     for (int e = t; e < 2 * DM * kT; e += kT) sXd[e] = 0.0;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(&tmem_slot)));
@@ -486,7 +509,6 @@ __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, i
     uint32_t phase = 0, xphase[2] = {0, 0};
     const uint64_t dBh = umma_desc(su32(sBh)), dBl = umma_desc(su32(sBl));
     const int64_t ntiles = (n + kT - 1) / kT;
-    // full tiles are prefetched with bulk async copies; the tail tile is loaded directly
     auto prefetch = [&](int64_t tile, int buf) {
         if (tile >= ntiles || (tile + 1) * kT > n) return;
         const uint32_t b = su32(&mbar_x[buf]);
@@ -494,7 +516,56 @@ __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, i
         for (int j = 0; j < D; ++j)
             bulk_g2s(su32(sXd + (buf * DM + j) * kT), X + (int64_t)j * ld + tile * kT, kT * 8, b);
     };
-    if (t == 0) prefetch(blockIdx.x, 0);
+    const int sub = t >> 7, row = t & 127;
+    // A-prep of `tile` from X buffer xb into the A operands and FP32 rows buffer xb
+    auto aprep = [&](int64_t tile, int xb) {
+        const int64_t i = tile * kT + t;
+        const bool valid = i < n;
+        const bool full = (tile + 1) * kT <= n;
+        if (full) {
+            mbar_wait(su32(&mbar_x[xb]), xphase[xb]);
+            xphase[xb] ^= 1;
+        }
+        unsigned char* ah = sAh + sub * kOpBytes;
+        unsigned char* al = sAl + sub * kOpBytes;
+        const double* xs = sXd + xb * DM * kT;
+        float* xr = sXr + (xb * kT + t) * kXR;
+#pragma unroll
+        for (int j = 0; j < DM; j += 4) {
+            float f[4];
+            uint32_t h[4], l[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                double xv;
+                if (full) xv = xs[(j + q) * kT + t];
+                else xv = (valid && j + q < D) ? __ldg(X + (int64_t)(j + q) * ld + i) : 0.0;
+                f[q] = (valid && j + q < D) ? (float)(xv - sC[j + q]) : 0.f;
+                h[q] = tf32(f[q]);
+                l[q] = tf32(f[q] - __uint_as_float(h[q]));
+            }
+            *reinterpret_cast<float4*>(xr + j) = make_float4(f[0], f[1], f[2], f[3]);
+            *reinterpret_cast<uint4*>(ah + op_off(row, j)) = make_uint4(h[0], h[1], h[2], h[3]);
+            *reinterpret_cast<uint4*>(al + op_off(row, j)) = make_uint4(l[0], l[1], l[2], l[3]);
+        }
+        proxy_fence();
+    };
+    auto issue_mma = [&]() {
+        tc_fence_after();
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2) {
+            const uint32_t d = tmem + 128 * s2;
+            const uint64_t dAh = umma_desc(su32(sAh + s2 * kOpBytes)), dAl = umma_desc(su32(sAl + s2 * kOpBytes));
+#pragma unroll
+            for (int ks = 0; ks < kKA / 8; ++ks) {
+                const uint64_t ko = (uint64_t)((2 * ks * kLBO) >> 4);
+                mma_tf32(d, dAh + ko, dBh + ko, ks > 0 ? 1u : 0u);
+                mma_tf32(d, dAh + ko, dBl + ko, 1u);
+                mma_tf32(d, dAl + ko, dBh + ko, 1u);
+            }
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                     : "memory");
+    };
 
     const int kw = warp;
     const bool mact = kw < K;
@@ -508,16 +579,15 @@ __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, i
     for (int j = 0; j < GramPairs::NSG; ++j) accs[j] = 0.f;
 #pragma unroll
     for (int j = 0; j < DM / 2; ++j) acc1[j] = 0;
-    int since_flush = 0;
     double ll_acc = 0.0;
     const unsigned lt_mask = (1u << lane) - 1u;
-    // flush: warp butterfly of each FP32 accumulator, lane (idx % 32) adds it to the FP64 shared total
     auto flush1 = [&](float v, int idx) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if ((idx & 31) == lane) sAcc[kw * C::NS + idx] += (double)v;
     };
     auto flush = [&]() {
+        __syncwarp();
         if (!mact) return;
         flush1(accn, 0);
         accn = 0.f;
@@ -532,7 +602,7 @@ __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, i
         int ip = 0, is = 0;
 #pragma unroll
         for (int a = 0; a < DM; ++a) {
-            const int base = 1 + DM + a * DM - (a * (a - 1)) / 2;  // packed index of (a, a)
+            const int base = 1 + DM + a * DM - (a * (a - 1)) / 2;
             if (a & 1) {
                 flush1(accs[is], base);
                 accs[is++] = 0.f;
@@ -547,66 +617,30 @@ __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, i
             }
         }
     };
-    const int sub = t >> 7, row = t & 127;
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
-    int buf = 0;
 
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t t0 = tile * kT;
-        const int64_t i = t0 + t;
-        const bool valid = i < n;
-        const bool full = t0 + kT <= n;
-        if (full) {
-            mbar_wait(su32(&mbar_x[buf]), xphase[buf]);
-            xphase[buf] ^= 1;
+    int64_t cur = blockIdx.x;
+    int xb = 0;
+    if (cur < ntiles) {
+        if (t == 0) {
+            prefetch(cur, 0);
+            prefetch(cur + gridDim.x, 1);
         }
-        // ---------------- operand A from the prefetched FP64 tile
-        unsigned char* ah = sAh + sub * kOpBytes;
-        unsigned char* al = sAl + sub * kOpBytes;
-        const double* xs = sXd + buf * DM * kT;
-#pragma unroll
-        for (int j = 0; j < DM; j += 4) {
-            float f[4];
-            uint32_t h[4], l[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                double xv;
-                if (full) xv = xs[(j + q) * kT + t];
-                else xv = (valid && j + q < D) ? __ldg(X + (int64_t)(j + q) * ld + i) : 0.0;
-                f[q] = (valid && j + q < D) ? (float)(xv - sC[j + q]) : 0.f;
-                sX[(j + q) * C::XS + t] = f[q];
-                h[q] = tf32(f[q]);
-                l[q] = tf32(f[q] - __uint_as_float(h[q]));
-            }
-            *reinterpret_cast<uint4*>(ah + op_off(row, j)) = make_uint4(h[0], h[1], h[2], h[3]);
-            *reinterpret_cast<uint4*>(al + op_off(row, j)) = make_uint4(l[0], l[1], l[2], l[3]);
-        }
-        proxy_fence();
+        aprep(cur, 0);
         tc_fence_before();
         __syncthreads();
-        if (t == 0) {
-            prefetch(tile + gridDim.x, buf ^ 1);  // buffer buf^1 was consumed one tile ago
-            tc_fence_after();
-#pragma unroll
-            for (int s2 = 0; s2 < 2; ++s2) {
-                const uint32_t d = tmem + 128 * s2;
-                const uint64_t dAh = umma_desc(su32(sAh + s2 * kOpBytes)), dAl = umma_desc(su32(sAl + s2 * kOpBytes));
-#pragma unroll
-                for (int ks = 0; ks < kKA / 8; ++ks) {
-                    const uint64_t ko = (uint64_t)((2 * ks * kLBO) >> 4);
-                    mma_tf32(d, dAh + ko, dBh + ko, ks > 0 ? 1u : 0u);
-                    mma_tf32(d, dAh + ko, dBl + ko, 1u);
-                    mma_tf32(d, dAl + ko, dBh + ko, 1u);
-                }
-            }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                         : "memory");
-        }
-        buf ^= 1;
+        if (t == 0) issue_mma();
+    }
+    while (cur < ntiles) {
+      // one flush site per super-tile of up to 64 tiles keeps the FP32
+      // partials short (<= 64*8 batches per lane) and the code compact
+      for (int st = 0; st < 64 && cur < ntiles; ++st) {
+        const int64_t next = cur + gridDim.x;
+        const bool valid = cur * kT + t < n;
         mbar_wait(bar, phase);
         phase ^= 1;
         tc_fence_after();
-        // ---------------- epilogue
+        // ---------------- epilogue(cur)
         float w[kKmax];
         float m = -INFINITY;
 #pragma unroll
@@ -631,60 +665,77 @@ __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, i
         for (int k = 0; k < kKmax; ++k) ssum += __expf(w[k] - m);
         const float ll = m + __logf(ssum);
         if (valid) ll_acc += (double)ll;
-        float g[kKmax];
-        unsigned rank[kKmax];
 #pragma unroll
         for (int k = 0; k < kKmax; ++k) {
-            g[k] = __expf(w[k] - ll);
-            const bool sig = valid && k < K && g[k] >= kGammaMin;
-            const unsigned b = __ballot_sync(0xffffffffu, sig);
-            rank[k] = sig ? __popc(b & lt_mask) : 0xffffffffu;
-            if (lane == 0) cnt[warp * 8 + k] = __popc(b);
+            const float gk = __expf(w[k] - ll);
+            sG[k * kT + t] = gk;
+            const unsigned b = __ballot_sync(0xffffffffu, valid && gk >= sThr[k]);
+            if (lane == 0) bal[warp * 8 + k] = b;
         }
         __syncthreads();
         if (t < kKmax) {
             int a2 = 0;
             for (int wv = 0; wv < 8; ++wv) {
                 off[wv * 8 + t] = a2;
-                a2 += cnt[wv * 8 + t];
+                a2 += __popc(bal[wv * 8 + t]);
             }
             tot[t] = a2;
         }
         __syncthreads();
-#pragma unroll
-        for (int k = 0; k < kKmax; ++k)
-            if (rank[k] != 0xffffffffu) {
-                const int p = off[warp * 8 + k] + (int)rank[k];
+#pragma unroll 1
+        for (int k = 0; k < kKmax; ++k) {
+            const unsigned b = bal[warp * 8 + k];
+            if ((b >> lane) & 1u) {
+                const int p = off[warp * 8 + k] + __popc(b & lt_mask);
                 lstT[k * kT + p] = (uint16_t)t;
-                lstG[k * kT + p] = g[k];
+                lstG[k * kT + p] = sG[k * kT + t];
             }
+        }
+        // ---------------- A-prep(next) overlaps nothing yet; MMA(next) then runs under M(cur)
+        if (next < ntiles) aprep(next, xb ^ 1);
+        tc_fence_before();
         __syncthreads();
-        // ---------------- M-phase: packed FP32 pairs
+        if (t == 0 && next < ntiles) {
+            prefetch(next + gridDim.x, xb);  // buffer xb was consumed by aprep(cur)
+            issue_mma();
+        }
+        // ---------------- M-phase(cur)
         if (mact) {
             const int nk = tot[kw];
-            const float* muk = sMu + kw * DM;
+            const float* nmu = sNMu + kw * DM;
+            uint64_t nm2[DM / 2];
+#pragma unroll
+            for (int mm = 0; mm < DM / 2; ++mm) nm2[mm] = pack2(nmu[2 * mm], nmu[2 * mm + 1]);
             for (int e0 = 0; e0 < nk; e0 += 32) {
                 const int e = e0 + lane;
                 const bool ve = e < nk;
                 const int tt = ve ? lstT[kw * kT + e] : 0;
                 const float gg = ve ? lstG[kw * kT + e] : 0.f;
-                float d[DM];
+                const float4* xr4 = reinterpret_cast<const float4*>(sXr + (xb * kT + tt) * kXR);
+                uint64_t d2[DM / 2], gd2[DM / 2];
 #pragma unroll
-                for (int a2 = 0; a2 < DM; ++a2) d[a2] = sX[a2 * C::XS + tt] - muk[a2];
-                uint64_t d2[DM / 2];
-#pragma unroll
-                for (int mm = 0; mm < DM / 2; ++mm) d2[mm] = pack2(d[2 * mm], d[2 * mm + 1]);
+                for (int q = 0; q < DM / 4; ++q) {
+                    const float4 v = xr4[q];
+                    d2[2 * q] = add2(pack2(v.x, v.y), nm2[2 * q]);
+                    d2[2 * q + 1] = add2(pack2(v.z, v.w), nm2[2 * q + 1]);
+                }
                 accn += gg;
                 const uint64_t g2 = pack2(gg, gg);
 #pragma unroll
-                for (int mm = 0; mm < DM / 2; ++mm) ffma2(acc1[mm], g2, d2[mm]);
+                for (int mm = 0; mm < DM / 2; ++mm) {
+                    gd2[mm] = mul2(g2, d2[mm]);
+                    acc1[mm] = add2(acc1[mm], gd2[mm]);
+                }
                 int ip = 0, is = 0;
 #pragma unroll
                 for (int a2 = 0; a2 < DM; ++a2) {
-                    const float ga = gg * d[a2];
+                    float gl, gh, dl, dh;
+                    unpack2(gd2[a2 / 2], gl, gh);
+                    unpack2(d2[a2 / 2], dl, dh);
+                    const float ga = (a2 & 1) ? gh : gl;
                     const uint64_t ga2 = pack2(ga, ga);
                     if (a2 & 1) {
-                        accs[is] = fmaf(ga, d[a2], accs[is]);
+                        accs[is] = fmaf(ga, dh, accs[is]);
                         ++is;
                     }
 #pragma unroll
@@ -693,15 +744,14 @@ __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, i
                         ++ip;
                     }
                 }
-                if (++since_flush == 128) {
-                    flush();
-                    since_flush = 0;
-                }
             }
         }
         __syncthreads();
+        cur = next;
+        xb ^= 1;
+      }
+      flush();
     }
-    flush();
     const double bl = block_sum_d(ll_acc, sRed);
     const int SK = stat_k(D), NE = K * SK;
     double* myp = partial + (int64_t)blockIdx.x * (NE + 1);
@@ -730,7 +780,7 @@ __global__ void __launch_bounds__(kT, 1) k_em_tc(const double* __restrict__ X, i
 static size_t em_tc_smem() {
     using C = FastCfg<16>;
     size_t b = (size_t)6 * kOpBytes + (size_t)2 * 16 * kT * 8;
-    b += (size_t)(kKmax * 16 + kKmax + 16 * C::XS + kKmax * kT) * 4;
+    b += (size_t)(2 * kT * kXR + kKmax * 16 + 2 * kKmax + 2 * kKmax * kT) * 4;
     b += (size_t)kKmax * kT * 2;
     b += (64 + 64 + 8) * 4;
     b = (b + 15) / 16 * 16;
