@@ -267,6 +267,10 @@ def run_ours(args):
     if rank != 0:
         return
     hbm, src = peaks()
+    tc = os.environ.get("ES_EM_KERNEL", "tc") != "simt" and ctx.precision == "mixed"
+    em_kernel = ("k_em_tc (tcgen05 3xTF32 whitening + FP32/FP64 M-step)" if tc else
+                 "k_em_fast<16> (SIMT FP32)" if ctx.precision == "mixed" else "k_em_team<16,2> (FP64)")
+    sc_kernel = "k_score_fast<16> (FP32 + FP64 refine)" if ctx.precision == "mixed" else "k_score_team<16> (FP64)"
     it_s = args.steps / (em_ms_max / 1e3)
     bytes_iter = n_global * D * 8
     em_kern_avg = kern_ms / max(kern_n, 1)
@@ -281,12 +285,15 @@ def run_ours(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (SYN-v1 seed 42, device generated)",
         "config": {"workload": WORKLOAD, "N": n_global, "D": D, "K": K, "covariance": "full", "init": "random seed 7",
                    "l2": "inputs (8.6 GB) larger than L2; no flush", "parallelism": f"rows sharded over {world} GPU(s)"},
-        "roofline": {"bound": "hbm", "kernel": "k_em_team<16,2>", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                     "frac": ach / hbm, "peak_source": src, "traffic": None,
+        "roofline": {"bound": "hbm", "kernel": em_kernel, "achieved": ach, "peak": hbm, "unit": "GB/s",
+                     "frac": ach / hbm, "peak_source": src, "traffic": args.traffic,
                      "algorithmic_bytes_per_launch": bytes_iter / world, "avg_launch_ms": em_kern_avg,
-                     "kernel_share_of_step": kern_ms / em_ms if em_ms else None},
+                     "kernel_share_of_step": kern_ms / em_ms if em_ms else None,
+                     "traffic_source": args.traffic_note,
+                     "limiter": "SIMT issue (M-step Gram ~4 significant (event, component) pairs/event, FP32 "
+                                "FFMA2) - see DESIGN.md Roofline"},
         "score": {"events_per_s": sc_evs, "ms_per_pass": sc_ms / args.steps, "n_flagged": nflag,
-                  "roofline": {"bound": "hbm", "kernel": "k_score_team<16>", "achieved": sc_ach, "peak": hbm,
+                  "roofline": {"bound": "hbm", "kernel": sc_kernel, "achieved": sc_ach, "peak": hbm,
                                "unit": "GB/s", "frac": sc_ach / hbm,
                                "algorithmic_bytes_per_launch": sc_bytes, "avg_launch_ms": sc_kern_avg}},
         "gpu_launches": em_launches,
@@ -308,6 +315,9 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override N (debug only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="dram bytes per EM launch from the committed ncu --set full capture (profiles/)")
+    ap.add_argument("--traffic-note", default=None)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

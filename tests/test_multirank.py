@@ -1,0 +1,78 @@
+"""world_size-2 coverage of the sharded path.
+
+CPU: the gloo exchange callbacks used by es_ctx_create_exchange (rank-ordered
+all-gather; sum/min/max in f64 and i64) through real ctypes function pointers.
+GPU: two ranks sharing cuda:0 run fit / calibrate / detect / k-means++ on the row
+shards of one SYN-v1 matrix and must reproduce the single-rank results.
+"""
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+WORKER = os.path.join(ROOT, "tests", "mp_worker.py")
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def launch(args, world=2, timeout=600):
+    port = free_port()
+    procs = []
+    for r in range(world):
+        env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(r), WORLD_SIZE=str(world),
+                   LOCAL_RANK="0")
+        procs.append(subprocess.Popen([sys.executable, WORKER, *args], env=env, stdout=subprocess.PIPE,
+                                      stderr=subprocess.STDOUT, text=True))
+    outs = [p.communicate(timeout=timeout)[0] for p in procs]
+    for p, o in zip(procs, outs):
+        assert p.returncode == 0, o
+
+
+def test_gloo_exchange_callbacks(tmp_path):
+    out = str(tmp_path / "ex")
+    launch(["exchange", out])
+    for r in range(2):
+        z = np.load(out + f".{r}.npz")
+        assert np.array_equal(z["gather"], np.concatenate([np.arange(5), np.arange(5) + 10]))
+        base = np.array([3, -1, 7])
+        assert np.array_equal(z["r00"], base * 3) and np.array_equal(z["r10"], base * 3)
+        assert np.array_equal(z["r01"], np.minimum(base, base * 2))
+        assert np.array_equal(z["r02"], np.maximum(base, base * 2))
+        assert z["r10"].dtype == np.int64
+
+
+@pytest.mark.gpu
+def test_two_ranks_match_single_rank(tmp_path):
+    import paper_2506_02007_b200 as es
+    n = 200_003
+    out = str(tmp_path / "fit")
+    launch(["fit", out, str(n)])
+    z0, z1 = np.load(out + ".0.npz"), np.load(out + ".1.npz")
+    # identical model on every rank (rank-ordered reduction)
+    for key in ("w", "mu", "cov", "per", "kmu"):
+        assert np.array_equal(z0[key], z1[key]), key
+    assert z1["off"] == n // 2
+    ds = es.Dataset.generate(42, n, 16, 8)
+    m = es.fit_em(ds, 8, init="random", tol=0.0, max_iter=8, seed=7)
+    assert np.allclose(z0["w"], m.weights, rtol=1e-9, atol=1e-12)
+    assert np.allclose(z0["mu"], m.means, rtol=1e-9, atol=1e-9)
+    assert np.allclose(z0["cov"], m.covariances, rtol=1e-9, atol=1e-9)
+    assert np.allclose(z0["per"], m.fit_report.per_iteration_log_likelihoods, rtol=1e-12)
+    d, ld = es.calibrate_threshold(m, ds, 0.01, n_train=n // 2, return_log=True)
+    assert abs(ld - float(z0["ld"])) <= 1e-9 * abs(ld)
+    r = es.detect(m, ds, log_delta=float(z0["ld"]))
+    both = np.concatenate([z0["idx"], z1["idx"]])
+    assert int(z0["nflag"]) == int(z1["nflag"]) == len(both)
+    assert len(np.setxor1d(both, r.anomaly_indices)) <= 2  # only threshold-band events may differ
+    mk = es.fit_em(ds, 4, init="kmeans++", tol=0.0, max_iter=3, seed=5)
+    assert np.allclose(z0["kmu"], mk.means, rtol=1e-9, atol=1e-9)
