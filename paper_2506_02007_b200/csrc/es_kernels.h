@@ -1,5 +1,6 @@
 // es_kernels.h — launchers for the sm_100a kernels (es_kernels.cu).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -81,6 +82,13 @@ void launch_em_fast(const double* X, int64_t n, int64_t ld, int D, int K, const 
 bool em_tc_enabled();
 void launch_em_tc(const double* X, int64_t n, int64_t ld, int D, int K, const double* model, const double* center,
                   double* partial, int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
+// Warp-specialized tcgen05 pass (es_ws.cu), the default (ES_EM_KERNEL=ws|tc|simt).
+bool em_ws_enabled();
+// xmap: 2-D TMA tensor map over the planar event matrix (box = 128 rows x D planes).
+void launch_em_ws(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model, const double* center,
+                  double* partial, int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
+// Builds that tensor map (driver entry point resolved through the runtime).
+bool make_event_tmap(CUtensorMap* map, const double* X, int64_t n, int64_t ld, int D);
 bool score_fast_supported(int D, int K, const ScoreOut& o);
 void launch_score_fast(const double* X, int64_t n, int64_t ld, int D, int K, const double* model,
                        const double* center, const ScoreOut& o, double* blocksum, int num_sms, int* nblk,

@@ -256,6 +256,8 @@ struct es_dataset {
     int64_t n_local = 0, n_global = 0, row_offset = 0, ld = 0;
     int D = 0;
     double* X = nullptr;
+    CUtensorMap xmap{};      // TMA descriptor over X (D <= 16), see make_event_tmap
+    bool has_xmap = false;
     ~es_dataset() {
         if (X) cudaFree(X);
     }
@@ -643,7 +645,10 @@ bool em_iterate(es_em_state* st) {
         double* part = c->partial.as<double>((size_t)std::max(em_grid(D, K, c->num_sms), c->num_sms) * NE1);
         c->t_begin();
         if (c->precision == 0 && em_fast_supported(D, K)) {
-            if (em_tc_enabled())
+            if (em_ws_enabled() && ds->has_xmap)
+                launch_em_ws(&ds->xmap, ds->n_local, D, K, dmodel, st->dcenter.as<double>(D), part, c->num_sms,
+                             &nblk, c->stream, c->ls);
+            else if (em_tc_enabled())
                 launch_em_tc(ds->X, ds->n_local, ds->ld, D, K, dmodel, st->dcenter.as<double>(D), part, c->num_sms,
                              &nblk, c->stream, c->ls);
             else
@@ -833,6 +838,7 @@ int es_ctx_kernel_time(es_ctx* c, int which, double* ms, int64_t* launches) {
 
 // -------------------------------------------------------------- dataset
 static void finish_dataset(es_ctx* c, es_dataset* ds) {
+    ds->has_xmap = ds->n_local > 0 && make_event_tmap(&ds->xmap, ds->X, ds->n_local, ds->ld, ds->D);
     double nl = (double)ds->n_local;
     std::vector<double> all = c->allgather_host(&nl, 1);
     int64_t off = 0, tot = 0;

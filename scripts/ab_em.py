@@ -14,6 +14,6 @@ prec = sys.argv[4] if len(sys.argv) > 4 else "mixed"
 ctx = es.Context(0, precision=prec)
 ds = es.Dataset.generate(42, n, D, K, ctx=ctx)
 m = es.fit_em(ds, K, init="random", tol=0.0, max_iter=5, seed=7)
-np.savez(f"gpurun_out/ab_{os.environ.get('ES_EM_KERNEL', 'tc')}_{prec}.npz", w=m.weights, mu=m.means,
+np.savez(f"gpurun_out/ab_{os.environ.get('ES_EM_KERNEL', 'ws')}_{prec}.npz", w=m.weights, mu=m.means,
          cov=m.covariances, per=m.fit_report.per_iteration_log_likelihoods)
-print(os.environ.get("ES_EM_KERNEL", "tc"), prec, m.fit_report.per_iteration_log_likelihoods)
+print(os.environ.get("ES_EM_KERNEL", "ws"), prec, m.fit_report.per_iteration_log_likelihoods)

@@ -21,5 +21,5 @@ for it in range(iters):
     lib.es_ctx_kernel_time(ctx.handle, 0, C.byref(ms), C.byref(cnt))
     out.append(ms.value)
 m = em.finish()
-print(os.environ.get("ES_EM_KERNEL", "tc"), prec, " ".join(f"{v:.2f}" for v in out))
+print(os.environ.get("ES_EM_KERNEL", "ws"), prec, " ".join(f"{v:.2f}" for v in out))
 print("weights", m.weights)

