@@ -1,13 +1,13 @@
 // es_ws.cu — warp-specialized fused EM pass (default for D <= 16, K <= 8).
 //
 // One CTA per SM, 12 warps in three warpgroups:
-//   WG0 (warps 0-3, 120 regs): producer.  Per 128-event tile: waits for the
+//   WG0 (warps 0-3, 104 regs): producer.  Per 128-event tile: waits for the
 //       bulk-prefetched FP64 tile, forms x' = x - c, writes the TF32 hi/lo UMMA
 //       operand and FP32 rows, issues 9 tcgen05.mma (3xTF32, K=24) into one of
 //       two TMEM accumulators, then runs the epilogue of the previous tile: one
 //       TMEM row per thread (= event), log-sum-exp over K, responsibilities,
 //       ballot-compacted per-component gamma lists into a ring slot.
-//   WG1-2 (warps 4-11, 192 regs): consumers.  Warp 4+k owns component k's
+//   WG1-2 (warps 4-11, 200 regs): consumers.  Warp 4+k owns component k's
 //       sufficient statistics in registers (packed FP32 pairs, FFMA2), walks its
 //       gamma list of every tile, and flushes into FP64 shared accumulators every
 //       64 tiles.
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_ws(const __grid_constant__ CUten
 
     if (warp < 4) {
         // ============================================================ producer
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 120;\n" ::: "memory");
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 104;\n" ::: "memory");
         const int p = t;  // tile row / TMEM lane
         const uint32_t lane_base = (uint32_t)(32 * warp) << 16;
         const unsigned lt_mask = (1u << lane) - 1u;
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_ws(const __grid_constant__ CUten
         S.red[p] = ll_acc;
     } else {
         // ============================================================ consumers
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 192;\n" ::: "memory");
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 200;\n" ::: "memory");
         const int kw = warp - 4;
         const bool mact = kw < K;
         uint64_t accp[NP];
@@ -312,14 +312,18 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_ws(const __grid_constant__ CUten
                 mbar_wait_sleep(su32(&S.full[j % RS]), (uint32_t)((j / RS) & 1));
                 const Ring& R = S.ring[j % RS];
                 if (mact) {
-#pragma unroll 1
-                    for (int sw = 0; sw < 4; ++sw) {
-                        const int nk = R.cnt[kw * 4 + sw];
-                        if (nk == 0) continue;
-                        const bool ve = lane < nk;
-                        const int e = (kw * 4 + sw) * 32 + lane;
-                        const int tt = ve ? R.lt[e] : 0;
-                        const float gg = ve ? R.lg[e] : 0.f;
+                    // the 4 producer-warp sub-lists, walked as one dense list
+                    const int c0 = R.cnt[kw * 4 + 0], c1 = R.cnt[kw * 4 + 1], c2 = R.cnt[kw * 4 + 2];
+                    const int p1 = c0, p2 = c0 + c1, p3 = c0 + c1 + c2;
+                    const int nk = p3 + R.cnt[kw * 4 + 3];
+                    for (int e0 = 0; e0 < nk; e0 += 32) {
+                        const int e = e0 + lane;
+                        const bool ve = e < nk;
+                        const int sw = (e >= p1) + (e >= p2) + (e >= p3);
+                        const int base = sw == 0 ? 0 : sw == 1 ? p1 : sw == 2 ? p2 : p3;
+                        const int ix = (kw * 4 + sw) * 32 + (e - base);
+                        const int tt = ve ? R.lt[ix] : 0;
+                        const float gg = ve ? R.lg[ix] : 0.f;
                         const float4* xr4 = reinterpret_cast<const float4*>(R.xr + tt * XR);
                         uint64_t d2[DM / 2];
 #pragma unroll
