@@ -89,6 +89,10 @@ void launch_em_ws(const CUtensorMap* xmap, int64_t n, int D, int K, const double
                   double* partial, int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
 // Builds that tensor map (driver entry point resolved through the runtime).
 bool make_event_tmap(CUtensorMap* map, const double* X, int64_t n, int64_t ld, int D);
+// tcgen05 scoring pass (es_score_tc.cu); ES_SCORE_KERNEL=simt selects k_score_fast.
+bool score_tc_supported(int D, int K, const ScoreOut& o);
+void launch_score_tc(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model, const double* center,
+                     const ScoreOut& o, double* blocksum, int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
 bool score_fast_supported(int D, int K, const ScoreOut& o);
 void launch_score_fast(const double* X, int64_t n, int64_t ld, int D, int K, const double* model,
                        const double* center, const ScoreOut& o, double* blocksum, int num_sms, int* nblk,

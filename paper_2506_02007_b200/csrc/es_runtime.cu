@@ -451,8 +451,10 @@ struct Out {
 
 // Scoring launch: mixed-precision kernel when supported, FP64 team kernel otherwise.
 void score_launch(es_ctx* c, const double* X, int64_t n, int64_t ld, int D, int K, const double* dmodel,
-                  const double* center, const ScoreOut& o, double* bs, int* nblk) {
-    if (c->precision == 0 && center && score_fast_supported(D, K, o))
+                  const double* center, const ScoreOut& o, double* bs, int* nblk, const CUtensorMap* xmap = nullptr) {
+    if (c->precision == 0 && center && xmap && score_tc_supported(D, K, o))
+        launch_score_tc(xmap, n, D, K, dmodel, center, o, bs, c->num_sms, nblk, c->stream, c->ls);
+    else if (c->precision == 0 && center && score_fast_supported(D, K, o))
         launch_score_fast(X, n, ld, D, K, dmodel, center, o, bs, c->num_sms, nblk, c->stream, c->ls);
     else
         launch_score(X, n, ld, D, K, dmodel, o, bs, c->num_sms, nblk, c->stream, c->ls);
@@ -467,7 +469,8 @@ double run_score(es_ctx* c, es_dataset* ds, const double* dmodel, int K, ScoreOu
     if (ds->n_local > 0) {
         int nblk = 0;
         c->t_begin();
-        score_launch(c, ds->X, ds->n_local, ds->ld, D, K, dmodel, center, o, bs, &nblk);
+        score_launch(c, ds->X, ds->n_local, ds->ld, D, K, dmodel, center, o, bs, &nblk,
+                     ds->has_xmap ? &ds->xmap : nullptr);
         c->t_end(c->score_ms, c->score_launches);
         double* red = c->scratch2.as<double>(2);
         launch_reduce_blocks(bs, nblk, 2, red, c->stream, c->ls);
@@ -1210,7 +1213,8 @@ int es_gmm_calibrate(es_ctx* c, es_dataset* ds, const es_gmm_params* p, int64_t 
             else o.best_ld = keys;
             int nblk = 0;
             double* bs = c->scratch.as<double>(score_blocks(c, ds->D, p->K));
-            score_launch(c, ds->X, nloc, ds->ld, ds->D, p->K, m, c->center.as<double>(ds->D), o, bs, &nblk);
+            score_launch(c, ds->X, nloc, ds->ld, ds->D, p->K, m, c->center.as<double>(ds->D), o, bs, &nblk,
+                         ds->has_xmap ? &ds->xmap : nullptr);
             c->check_launch();
         }
         // q-quantile, linear interpolation between order statistics, h = (n-1) q

@@ -1,0 +1,335 @@
+// es_score_tc.cu — tensor-core scoring pass (score_samples / predict / detect).
+//
+// Per 256-event tile (8 warps, thread per event):
+//   TMA 2-D tensor copy of the FP64 tile (prefetched one tile ahead)
+//   -> x' = x - c, TF32 hi/lo operand -> 2 x 9 tcgen05.mma (3xTF32, K = 24)
+//   -> TMEM epilogue: FP32 log densities of all K components
+//   -> FP64 recomputation of the candidate components (within 20 nats of the
+//      weighted best, or within FP32 rounding of the unweighted best) by
+//      per-lane refine slots reading x from the same shared tile
+//   -> ll, predict, best_k, best_logdens, flag (FP64-exact where it matters).
+// The MMA of tile j+1 is issued before the FP64 refinement of tile j, so the
+// tensor cores and the TMA engine run under the FP64 work.
+#include <cmath>
+#include <cstdlib>
+
+#include "es_kernels.h"
+#include "es_tc.cuh"
+
+namespace es {
+
+namespace {
+
+using namespace tc;
+
+constexpr int DM = 16;
+constexpr int KMAX = 8;
+constexpr int TT = 256;             // events per tile
+constexpr int W64S = DM * DM + 2;   // FP64 W stride (bank skew between components)
+
+struct SmemS {
+    unsigned char Bh[kOpBytes], Bl[kOpBytes];
+    unsigned char Ah[2][kOpBytes], Al[2][kOpBytes];   // [sub-tile]
+    double xd[3][DM * TT];                            // TMA tiles (planar), triple-buffered
+    double lnv[KMAX * TT];                            // FP64 log densities of refined (k, event)
+    uint16_t cev[KMAX * TT];                          // compacted candidate list: event
+    uint8_t ccomp[KMAX * TT];                         //                            component
+    int wcnt[8], woff[8], ncand;
+    double W64[KMAX * W64S];
+    double mu64[KMAX * (DM + 2)];
+    double ln64[KMAX], lp64[KMAX];
+    double c[DM];
+    double red[TT];
+    float cst[KMAX], lnf[KMAX];
+    uint64_t xfull[3], mma_done;
+    uint32_t tmem;
+};
+
+}  // namespace
+
+__global__ void __launch_bounds__(TT, 1) k_score_tc(const __grid_constant__ CUtensorMap xmap, int64_t n, int D, int K,
+                                                     const double* __restrict__ model,
+                                                     const double* __restrict__ center, ScoreOut o,
+                                                     double* __restrict__ blocksum) {
+    extern __shared__ __align__(1024) unsigned char smraw[];
+    SmemS& S = *reinterpret_cast<SmemS*>(smraw);
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    ModelView mv{K, D, const_cast<double*>(model)};
+    const int64_t ntiles = (n + TT - 1) / TT;
+    const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+    for (int j = t; j < DM; j += TT) S.c[j] = j < D ? center[j] : 0.0;
+    __syncthreads();
+    for (int e = t; e < kTileRows * kKA; e += TT) {
+        const int row = e / kKA, kk = e % kKA, k = row / DM, r = row % DM;
+        double v = 0.0;
+        if (k < K && r < D) {
+            const double* Wr = mv.W() + (int64_t)k * D * D + (int64_t)r * D;
+            if (kk < D) {
+                v = Wr[kk];
+            } else if (kk == DM) {
+                double b = 0.0;
+                for (int j = 0; j <= r; ++j) b = fma(Wr[j], mv.mu()[k * D + j] - S.c[j], b);
+                v = -b;
+            }
+        }
+        const uint32_t h = tf32((float)v);
+        const uint32_t l = tf32((float)(v - (double)__uint_as_float(h)));
+        *reinterpret_cast<uint32_t*>(S.Bh + op_off(row, kk)) = h;
+        *reinterpret_cast<uint32_t*>(S.Bl + op_off(row, kk)) = l;
+    }
+    for (int e = t; e < 2 * kTileRows * (kKA - DM); e += TT) {
+        const int b2 = e / (kTileRows * (kKA - DM)), rr = e % (kTileRows * (kKA - DM));
+        const int row = rr / (kKA - DM), kk = DM + rr % (kKA - DM);
+        *reinterpret_cast<uint32_t*>(S.Ah[b2] + op_off(row, kk)) = kk == DM ? 0x3F800000u : 0u;
+        *reinterpret_cast<uint32_t*>(S.Al[b2] + op_off(row, kk)) = 0u;
+    }
+    for (int e = t; e < KMAX * DM * DM; e += TT) {
+        const int k = e / (DM * DM), rc = e % (DM * DM), r = rc / DM, cc = rc % DM;
+        S.W64[k * W64S + rc] = (k < K && r < D && cc < D) ? mv.W()[(int64_t)k * D * D + r * D + cc] : 0.0;
+    }
+    for (int e = t; e < KMAX * DM; e += TT) {
+        const int k = e / DM, j = e % DM;
+        S.mu64[k * (DM + 2) + j] = (k < K && j < D) ? mv.mu()[k * D + j] : 0.0;
+    }
+    for (int k = t; k < KMAX; k += TT) {
+        S.ln64[k] = k < K ? mv.lognorm()[k] : 0.0;
+        S.lp64[k] = k < K ? mv.logpi()[k] : -INFINITY;
+        S.cst[k] = k < K ? (float)(mv.logpi()[k] + mv.lognorm()[k]) : -INFINITY;
+        S.lnf[k] = k < K ? (float)mv.lognorm()[k] : -INFINITY;
+    }
+    for (int e = t; e < 3 * DM * TT; e += TT) (&S.xd[0][0])[e] = 0.0;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(&S.tmem)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (t == 0) {
+        for (int b = 0; b < 3; ++b) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&S.xfull[b])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&S.mma_done)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = S.tmem;
+    const uint64_t dBh = umma_desc(su32(S.Bh)), dBl = umma_desc(su32(S.Bl));
+    const int sub = t >> 7, row = t & 127;
+    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    auto tile_of = [&](int64_t j) { return (int64_t)blockIdx.x + j * gridDim.x; };
+    auto prefetch = [&](int64_t j) {  // two 128-row boxes per 256-event tile
+        if (j >= my_tiles) return;
+        const int s = (int)(j % 3);
+        const int r0 = (int)(tile_of(j) * TT);
+        mbar_expect_tx(su32(&S.xfull[s]), (uint32_t)(2 * D * 128 * 8));
+        // box = 128 rows x D planes lands as [plane][128]; place the halves at [plane][0..127] / [plane][128..255]
+        // by loading each 128-row half into its own [D][128] sub-buffer
+        tma_load_2d(su32(&S.xd[s][0]), &xmap, r0, 0, su32(&S.xfull[s]));
+        tma_load_2d(su32(&S.xd[s][DM * 128]), &xmap, r0 + 128, 0, su32(&S.xfull[s]));
+    };
+    // x of (tile buffer s, event t): half h = t/128 lives at xd[s][h*DM*128 + plane*128 + (t%128)]
+    auto xat = [&](int s, int plane) -> double { return S.xd[s][sub * DM * 128 + plane * 128 + row]; };
+    auto aprep_and_mma = [&](int64_t j) {
+        const int s = (int)(j % 3);
+        mbar_wait(su32(&S.xfull[s]), (uint32_t)((j / 3) & 1));
+        const bool valid = tile_of(j) * TT + t < n;
+#pragma unroll
+        for (int jj = 0; jj < DM; jj += 4) {
+            uint32_t h[4], l[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float f = (valid && jj + q < D) ? (float)(xat(s, jj + q) - S.c[jj + q]) : 0.f;
+                h[q] = tf32(f);
+                l[q] = tf32(f - __uint_as_float(h[q]));
+            }
+            *reinterpret_cast<uint4*>(S.Ah[sub] + op_off(row, jj)) = make_uint4(h[0], h[1], h[2], h[3]);
+            *reinterpret_cast<uint4*>(S.Al[sub] + op_off(row, jj)) = make_uint4(l[0], l[1], l[2], l[3]);
+        }
+        proxy_fence();
+        tc_fence_before();
+        __syncthreads();
+        if (t == 0) {
+            tc_fence_after();
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+                const uint32_t d = tmem + 128 * s2;
+                const uint64_t dAh = umma_desc(su32(S.Ah[s2])), dAl = umma_desc(su32(S.Al[s2]));
+#pragma unroll
+                for (int ks = 0; ks < kKA / 8; ++ks) {
+                    const uint64_t ko = (uint64_t)((2 * ks * kLBO) >> 4);
+                    mma_tf32(d, dAh + ko, dBh + ko, ks > 0 ? 1u : 0u);
+                    mma_tf32(d, dAh + ko, dBl + ko, 1u);
+                    mma_tf32(d, dAl + ko, dBh + ko, 1u);
+                }
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             su32(&S.mma_done))
+                         : "memory");
+        }
+    };
+
+    double ll_acc = 0.0, nflag = 0.0;
+    if (my_tiles > 0) {
+        if (t == 0) {
+            prefetch(0);
+            prefetch(1);
+        }
+        aprep_and_mma(0);
+    }
+    const unsigned lt_mask = (1u << lane) - 1u;
+    for (int64_t j = 0; j < my_tiles; ++j) {
+        const int s = (int)(j % 3);
+        const int64_t i = tile_of(j) * TT + t;
+        const bool valid = i < n;
+        mbar_wait(su32(&S.mma_done), (uint32_t)(j & 1));
+        tc_fence_after();
+        float w[KMAX], ln[KMAX];
+        float m = -INFINITY, bl = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) {
+            float u[16];
+            tmem_ld16(tmem + lane_base + 128 * sub + 16 * k, u);
+            tmem_wait_ld();
+            uint64_t q2 = 0;
+#pragma unroll
+            for (int r = 0; r < 16; r += 2) {
+                const uint64_t uu = pack2(u[r], u[r + 1]);
+                ffma2(q2, uu, uu);
+            }
+            float qa, qb;
+            unpack2(q2, qa, qb);
+            const float q = qa + qb;
+            ln[k] = S.lnf[k] - 0.5f * q;
+            w[k] = S.cst[k] - 0.5f * q;
+            m = fmaxf(m, w[k]);
+            bl = fmaxf(bl, ln[k]);
+        }
+        tc_fence_before();
+        // candidates needing FP64: responsibility above 1e-6 (FP32 error then moves ll by
+        // < 1e-6 * 1e-3 relative), or within FP32 rounding of either argmax
+        unsigned cand = 0;
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) {
+            const float tol = 1e-3f * (1.f + fabsf(w[k]));
+            if (valid && k < K && (w[k] >= m - 13.9f || ln[k] >= bl - tol)) cand |= 1u << k;
+        }
+        // deterministic compaction of (event, component) candidates
+        int mine = __popc(cand);
+        int incl = mine;
+#pragma unroll
+        for (int o2 = 1; o2 < 32; o2 <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o2);
+            if (lane >= o2) incl += v;
+        }
+        if (lane == 31) S.wcnt[warp] = incl;
+        __syncthreads();  // TMEM drained; A operand free; wcnt visible
+        if (t == 0) {
+            int a2 = 0;
+            for (int wv = 0; wv < 8; ++wv) {
+                S.woff[wv] = a2;
+                a2 += S.wcnt[wv];
+            }
+            S.ncand = a2;
+            prefetch(j + 2);
+        }
+        __syncthreads();
+        {
+            int pos = S.woff[warp] + incl - mine;
+            unsigned rem = cand;
+            while (rem) {
+                const int k = __ffs(rem) - 1;
+                rem &= rem - 1;
+                S.cev[pos] = (uint16_t)t;
+                S.ccomp[pos] = (uint8_t)k;
+                ++pos;
+            }
+        }
+        __syncthreads();
+        if (j + 1 < my_tiles) aprep_and_mma(j + 1);  // MMA(j+1) overlaps the FP64 refinement of tile j
+        // FP64 refinement, one (event, component) pair per thread at a time
+        const int nc = S.ncand;
+        for (int pidx = t; pidx < nc; pidx += TT) {
+            const int ev = S.cev[pidx], k = S.ccomp[pidx];
+            const double* Wk = S.W64 + k * W64S;
+            const double* mk = S.mu64 + k * (DM + 2);
+            const int h = ev >> 7, rw = ev & 127;
+            double dd[DM];
+#pragma unroll
+            for (int jj = 0; jj < DM; ++jj) dd[jj] = S.xd[s][h * DM * 128 + jj * 128 + rw] - mk[jj];
+            double q = 0.0;
+#pragma unroll
+            for (int r = 0; r < DM; ++r) {
+                double a = 0.0;
+#pragma unroll
+                for (int jj = 0; jj <= r; ++jj) a = fma(Wk[r * DM + jj], dd[jj], a);
+                q = fma(a, a, q);
+            }
+            S.lnv[k * TT + ev] = S.ln64[k] - 0.5 * q;
+        }
+        __syncthreads();
+        double mm = -INFINITY, bb = -INFINITY;
+        int am = 0, ab = 0;
+        double w64[KMAX];
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) {
+            const double l = ((cand >> k) & 1u) ? S.lnv[k * TT + t] : (double)ln[k];
+            w64[k] = S.lp64[k] + l;
+            if (k >= K) continue;
+            if (w64[k] > mm) { mm = w64[k]; am = k; }
+            if (l > bb) { bb = l; ab = k; }
+        }
+        double ss = 0.0;
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+            if (k < K) ss += exp(w64[k] - mm);
+        const double lld = mm + log(ss);
+        if (valid) {
+            ll_acc += lld;
+            const uint8_t f = ((o.mode == 1) ? lld : bb) < o.log_delta ? 1 : 0;
+            nflag += f;
+            if (o.ll) o.ll[i] = lld;
+            if (o.predict) o.predict[i] = am;
+            if (o.best_k) o.best_k[i] = ab;
+            if (o.best_ld) o.best_ld[i] = bb;
+            if (o.flags) o.flags[i] = f;
+        }
+    }
+    S.red[t] = ll_acc;
+    __syncthreads();
+    for (int st = TT / 2; st > 0; st >>= 1) {
+        if (t < st) S.red[t] += S.red[t + st];
+        __syncthreads();
+    }
+    if (t == 0) blocksum[2 * blockIdx.x] = S.red[0];
+    __syncthreads();
+    S.red[t] = nflag;
+    __syncthreads();
+    for (int st = TT / 2; st > 0; st >>= 1) {
+        if (t < st) S.red[t] += S.red[t + st];
+        __syncthreads();
+    }
+    if (t == 0) blocksum[2 * blockIdx.x + 1] = S.red[0];
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+bool score_tc_supported(int D, int K, const ScoreOut& o) {
+    const char* e = getenv("ES_SCORE_KERNEL");
+    if (e && e[0] == 's') return false;  // "simt" selects k_score_fast
+    return D <= 16 && K <= KMAX && !o.gamma && !o.lnk;
+}
+
+void launch_score_tc(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model, const double* center,
+                     const ScoreOut& o, double* blocksum, int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls) {
+    *nblk = num_sms;
+    const size_t smem = sizeof(SmemS) + 1024;
+    static bool a = false;
+    if (!a) {
+        cudaFuncSetAttribute(k_score_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        a = true;
+    }
+    k_score_tc<<<num_sms, TT, smem, s>>>(*xmap, n, D, K, model, center, o, blocksum);
+    ++ls.launches;
+}
+
+}  // namespace es

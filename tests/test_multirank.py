@@ -72,7 +72,7 @@ def test_two_ranks_match_single_rank(tmp_path):
                                                                          np.abs(m.means[k]).max()))
         assert np.all(np.abs(z0["cov"][k] - m.covariances[k]) <= 1e-5 * np.maximum(np.abs(m.covariances[k]),
                                                                                 np.abs(m.covariances[k]).max()))
-    assert np.allclose(z0["per"], m.fit_report.per_iteration_log_likelihoods, rtol=1e-8)
+    assert np.allclose(z0["per"], m.fit_report.per_iteration_log_likelihoods, rtol=1e-7)
     d, ld = es.calibrate_threshold(m, ds, 0.01, n_train=n // 2, return_log=True)
     assert abs(ld - float(z0["ld"])) <= 1e-6 * abs(ld)
     r = es.detect(m, ds, log_delta=float(z0["ld"]))
