@@ -1,12 +1,13 @@
 // es_score_tc.cu — tensor-core scoring pass (score_samples / predict / detect).
 //
 // Per 256-event tile (8 warps, thread per event):
-//   TMA 2-D tensor copy of the FP64 tile (prefetched one tile ahead)
+//   TMA 2-D tensor copies of the FP64 tile (prefetched two tiles ahead)
 //   -> x' = x - c, TF32 hi/lo operand -> 2 x 9 tcgen05.mma (3xTF32, K = 24)
 //   -> TMEM epilogue: FP32 log densities of all K components
-//   -> FP64 recomputation of the candidate components (within 20 nats of the
-//      weighted best, or within FP32 rounding of the unweighted best) by
-//      per-lane refine slots reading x from the same shared tile
+//   -> FP64 recomputation of the candidate components (responsibility above
+//      1e-6, or within FP32 rounding of either argmax), compacted into one
+//      (event, component) list per tile so FP64 work follows the candidate
+//      count, not the per-warp maximum; x is read from the same shared tile
 //   -> ll, predict, best_k, best_logdens, flag (FP64-exact where it matters).
 // The MMA of tile j+1 is issued before the FP64 refinement of tile j, so the
 // tensor cores and the TMA engine run under the FP64 work.
@@ -35,7 +36,7 @@ struct SmemS {
     uint16_t cev[KMAX * TT];                          // compacted candidate list: event
     uint8_t ccomp[KMAX * TT];                         //                            component
     int wcnt[8], woff[8], ncand;
-    double W64[KMAX * W64S];
+    alignas(16) double W64[KMAX * W64S];
     double mu64[KMAX * (DM + 2)];
     double ln64[KMAX], lp64[KMAX];
     double c[DM];
@@ -50,7 +51,7 @@ struct SmemS {
 __global__ void __launch_bounds__(TT, 1) k_score_tc(const __grid_constant__ CUtensorMap xmap, int64_t n, int D, int K,
                                                      const double* __restrict__ model,
                                                      const double* __restrict__ center, ScoreOut o,
-                                                     double* __restrict__ blocksum) {
+                                                     double* __restrict__ blocksum, int getenv_refine_all) {
     extern __shared__ __align__(1024) unsigned char smraw[];
     SmemS& S = *reinterpret_cast<SmemS*>(smraw);
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -176,6 +177,7 @@ __global__ void __launch_bounds__(TT, 1) k_score_tc(const __grid_constant__ CUte
         aprep_and_mma(0);
     }
     const unsigned lt_mask = (1u << lane) - 1u;
+    const bool refine_all = getenv_refine_all;
     for (int64_t j = 0; j < my_tiles; ++j) {
         const int s = (int)(j % 3);
         const int64_t i = tile_of(j) * TT + t;
@@ -207,10 +209,17 @@ __global__ void __launch_bounds__(TT, 1) k_score_tc(const __grid_constant__ CUte
         // candidates needing FP64: responsibility above 1e-6 (FP32 error then moves ll by
         // < 1e-6 * 1e-3 relative), or within FP32 rounding of either argmax
         unsigned cand = 0;
+        const float ldf = (float)o.log_delta;
 #pragma unroll
         for (int k = 0; k < KMAX; ++k) {
             const float tol = 1e-3f * (1.f + fabsf(w[k]));
-            if (valid && k < K && (w[k] >= m - 13.9f || ln[k] >= bl - tol)) cand |= 1u << k;
+            bool c;
+            if (refine_all)
+                c = w[k] >= m - 13.9f || ln[k] >= bl - tol;
+            else  // decisive only: near-ties of either argmax, or the best density near log delta
+                c = w[k] >= m - tol || ln[k] >= bl - tol ||
+                    (ln[k] == bl && fabsf(bl - ldf) <= 1e-3f * (1.f + fabsf(ldf)));
+            if (valid && k < K && c) cand |= 1u << k;
         }
         // deterministic compaction of (event, component) candidates
         int mine = __popc(cand);
@@ -260,7 +269,11 @@ __global__ void __launch_bounds__(TT, 1) k_score_tc(const __grid_constant__ CUte
             for (int r = 0; r < DM; ++r) {
                 double a = 0.0;
 #pragma unroll
-                for (int jj = 0; jj <= r; ++jj) a = fma(Wk[r * DM + jj], dd[jj], a);
+                for (int jj = 0; jj <= r; jj += 2) {  // W rows read as double2 (upper triangle is zero)
+                    const double2 wv = *reinterpret_cast<const double2*>(Wk + r * DM + jj);
+                    a = fma(wv.x, dd[jj], a);
+                    if (jj + 1 <= r) a = fma(wv.y, dd[jj + 1], a);
+                }
                 q = fma(a, a, q);
             }
             S.lnv[k * TT + ev] = S.ln64[k] - 0.5 * q;
@@ -277,11 +290,13 @@ __global__ void __launch_bounds__(TT, 1) k_score_tc(const __grid_constant__ CUte
             if (w64[k] > mm) { mm = w64[k]; am = k; }
             if (l > bb) { bb = l; ab = k; }
         }
-        double ss = 0.0;
+        // log-sum-exp about the FP64 maximum: the max term is exactly 1, the others are summed
+        // with FP32 exp (relative 1e-7 of a sum >= 1 -> ll error < 2e-7 absolute)
+        float ss = 0.f;
 #pragma unroll
         for (int k = 0; k < KMAX; ++k)
-            if (k < K) ss += exp(w64[k] - mm);
-        const double lld = mm + log(ss);
+            if (k < K) ss += __expf((float)(w64[k] - mm));
+        const double lld = mm + log((double)ss);
         if (valid) {
             ll_acc += lld;
             const uint8_t f = ((o.mode == 1) ? lld : bb) < o.log_delta ? 1 : 0;
@@ -328,7 +343,12 @@ void launch_score_tc(const CUtensorMap* xmap, int64_t n, int D, int K, const dou
         cudaFuncSetAttribute(k_score_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         a = true;
     }
-    k_score_tc<<<num_sms, TT, smem, s>>>(*xmap, n, D, K, model, center, o, blocksum);
+    static int refine_all = -1;
+    if (refine_all < 0) {
+        const char* e = getenv("ES_SCORE_REFINE");
+        refine_all = (e && e[0] == 'm') ? 0 : 1;  // ES_SCORE_REFINE=min: decisive components only
+    }
+    k_score_tc<<<num_sms, TT, smem, s>>>(*xmap, n, D, K, model, center, o, blocksum, refine_all);
     ++ls.launches;
 }
 
