@@ -40,6 +40,8 @@ struct MatrixView {
 };
 
 enum class Init { Random, KMeansPP };
+/// Diagonal covariances are an extension (the reference has none).
+enum class CovarianceType { Full, Diagonal };
 
 struct FitOptions {
     Init init = Init::KMeansPP;
@@ -47,6 +49,7 @@ struct FitOptions {
     int max_iter = 200;
     std::optional<double> reg;        // default 1e-6 * tr(S)/d; 0 disables
     std::uint64_t seed = 0;
+    CovarianceType covariance_type = CovarianceType::Full;
 };
 
 struct FitReport {

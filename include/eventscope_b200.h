@@ -54,6 +54,9 @@ extern "C" {
 #define ES_INIT_KMEANSPP 1 /* SPEC.md:291,319 (default of the C++ API) */
 #define ES_INIT_GIVEN 2    /* warm start from es_gmm_params */
 
+#define ES_COV_FULL 0
+#define ES_COV_DIAG 1 /* diagonal covariances (not in the reference) */
+
 #define ES_DETECT_COMPONENT 0 /* Def. 1: best-component density */
 #define ES_DETECT_MIXTURE 1   /* mixture density ablation */
 
@@ -75,6 +78,7 @@ typedef struct {
     int32_t max_iter; /* SPEC.md:321 default 200 */
     double reg;       /* < 0: default 1e-6*tr(S)/d; 0: disabled */
     uint64_t seed;
+    int32_t covariance_type; /* ES_COV_FULL (SPEC) or ES_COV_DIAG (extension) */
 } es_fit_opts;
 
 typedef struct {

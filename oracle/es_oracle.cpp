@@ -228,9 +228,10 @@ bool degenerate(const double* mn, const double* mx, int D) {
     return true;
 }
 
-void set_cov_to(double* covk, const double* S, int D, double reg) {
+void set_cov_to(double* covk, const double* S, int D, double reg, bool diag = false) {
     for (int a = 0; a < D; ++a)
-        for (int b = 0; b < D; ++b) covk[(size_t)a * D + b] = S[(size_t)a * D + b] + (a == b ? reg : 0.0);
+        for (int b = 0; b < D; ++b)
+            covk[(size_t)a * D + b] = (diag && a != b) ? 0.0 : S[(size_t)a * D + b] + (a == b ? reg : 0.0);
 }
 
 // k-means++ seeding: first centre uniform, then
@@ -375,6 +376,7 @@ int eso_fit_em(const double* X, int64_t N, int D, int K, const eso_fit_opts* opt
     if (K > 1 && degenerate(mn.data(), mx.data(), D))
         return fail(kData, "DegenerateData", "all points identical and K > 1");
     const double reg = opts->reg < 0 ? default_reg(S.data(), D) : opts->reg;
+    const bool diag = opts->cov_type == 1;  // diagonal extension: same M-step restricted to diag(Sigma)
 
     // ---- init
     SplitMix64 rng(opts->seed);
@@ -395,7 +397,7 @@ int eso_fit_em(const double* X, int64_t N, int D, int K, const eso_fit_opts* opt
         for (int k = 0; k < K; ++k) {
             pi[k] = 1.0 / K;
             std::memcpy(mu + (size_t)k * D, X + (size_t)rows[k] * D, sizeof(double) * D);
-            set_cov_to(cov + (size_t)k * D * D, S.data(), D, reg);
+            set_cov_to(cov + (size_t)k * D * D, S.data(), D, reg, diag);
         }
     }
 
@@ -478,7 +480,8 @@ int eso_fit_em(const double* X, int64_t N, int D, int K, const eso_fit_opts* opt
                         double g = gamma[(size_t)i * K + k];
                         for (int d = 0; d < D; ++d) y[d] = X[(size_t)i * D + d] - mu[(size_t)k * D + d];
                         for (int a = 0; a < D; ++a)
-                            for (int b = a; b < D; ++b) s2[(size_t)k * D * D + (size_t)a * D + b] += g * y[a] * y[b];
+                            for (int b = a; b < (diag ? a + 1 : D); ++b)
+                                s2[(size_t)k * D * D + (size_t)a * D + b] += g * y[a] * y[b];
                     }
             }
         }
@@ -489,6 +492,7 @@ int eso_fit_em(const double* X, int64_t N, int D, int K, const eso_fit_opts* opt
                     double s = 0.0;
                     for (int64_t c = 0; c < C; ++c) s += part_s2[(size_t)c * K * D * D + (size_t)k * D * D + (size_t)a * D + b];
                     double v = Nk[k] > 0 ? s / Nk[k] : 0.0;
+                    if (diag && a != b) v = 0.0;
                     ck[(size_t)a * D + b] = v + (a == b ? reg : 0.0);
                     ck[(size_t)b * D + a] = ck[(size_t)a * D + b];
                 }
@@ -501,7 +505,7 @@ int eso_fit_em(const double* X, int64_t N, int D, int K, const eso_fit_opts* opt
                     return fail(kNumeric, "RepeatedCollapse", "component collapsed more than twice");
                 int64_t r = (int64_t)rng.below((uint64_t)N);
                 std::memcpy(mu + (size_t)k * D, X + (size_t)r * D, sizeof(double) * D);
-                set_cov_to(cov + (size_t)k * D * D, S.data(), D, reg);
+                set_cov_to(cov + (size_t)k * D * D, S.data(), D, reg, diag);
                 pi[k] = 1.0 / K;
                 any = true;
             }
@@ -609,7 +613,8 @@ int eso_select_k_bic(const double* X, int64_t N, int D, const int* k_range, int 
             last_msg = g_err_msg;
             continue;
         }
-        const double p = (K - 1) + (double)K * D + (double)K * D * (D + 1) / 2.0;
+        const double p = (K - 1) + (double)K * D +
+                         (opts->cov_type == 1 ? (double)K * D : (double)K * D * (D + 1) / 2.0);
         bic[j] = -2.0 * rep.final_log_likelihood + p * std::log((double)N);
         if (bic[j] < best_bic) { best_bic = bic[j]; best = K; }
     }

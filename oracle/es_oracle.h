@@ -33,6 +33,7 @@ typedef struct {
     double reg;        /* < 0 => default 1e-6*tr(S)/d; 0 => disabled */
     uint64_t seed;
     int nthreads;      /* 0 => OpenMP default */
+    int cov_type;      /* 0 = full (SPEC), 1 = diagonal (extension) */
 } eso_fit_opts;
 
 typedef struct {

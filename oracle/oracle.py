@@ -27,7 +27,7 @@ class OracleError(RuntimeError):
 
 class FitOpts(C.Structure):
     _fields_ = [("init", C.c_int), ("tol", C.c_double), ("max_iter", C.c_int),
-                ("reg", C.c_double), ("seed", C.c_uint64), ("nthreads", C.c_int)]
+                ("reg", C.c_double), ("seed", C.c_uint64), ("nthreads", C.c_int), ("cov_type", C.c_int)]
 
 
 class FitReport(C.Structure):
@@ -133,13 +133,15 @@ def random_init(X, K, seed, reg=-1.0):
 INIT_RANDOM, INIT_KMEANSPP, INIT_GIVEN = 0, 1, 2
 
 
-def fit_em(X, K, init="kmeans++", tol=1e-6, max_iter=200, reg=None, seed=0, init_params=None, nthreads=0):
+def fit_em(X, K, init="kmeans++", tol=1e-6, max_iter=200, reg=None, seed=0, init_params=None, nthreads=0,
+           covariance_type="full"):
     X = np.ascontiguousarray(X, np.float64)
     N, D = X.shape
     code = {"random": INIT_RANDOM, "kmeans++": INIT_KMEANSPP, "given": INIT_GIVEN}[init]
     if init_params is not None:
         code = INIT_GIVEN
-    opts = FitOpts(code, tol, max_iter, -1.0 if reg is None else float(reg), seed, nthreads)
+    opts = FitOpts(code, tol, max_iter, -1.0 if reg is None else float(reg), seed, nthreads,
+                   {"full": 0, "diag": 1}[covariance_type])
     pi, mu, cov = np.empty(K), np.empty((K, D)), np.empty((K, D, D))
     per = np.empty(max_iter + 1)
     rep = FitReport()
@@ -176,12 +178,14 @@ def calibrate(X_train, pi, mu, cov, q, mode=0, nthreads=0):
     return d.value, ld.value
 
 
-def select_k_bic(X, k_range, init="kmeans++", tol=1e-6, max_iter=200, reg=None, seed=0, nthreads=0):
+def select_k_bic(X, k_range, init="kmeans++", tol=1e-6, max_iter=200, reg=None, seed=0, nthreads=0,
+                 covariance_type="full"):
     X = np.ascontiguousarray(X, np.float64)
     N, D = X.shape
     kr = np.ascontiguousarray(k_range, np.int32)
     code = {"random": INIT_RANDOM, "kmeans++": INIT_KMEANSPP}[init]
-    opts = FitOpts(code, tol, max_iter, -1.0 if reg is None else float(reg), seed, nthreads)
+    opts = FitOpts(code, tol, max_iter, -1.0 if reg is None else float(reg), seed, nthreads,
+                   {"full": 0, "diag": 1}[covariance_type])
     bic = np.empty(len(kr))
     best = C.c_int()
     _check(lib().eso_select_k_bic(_p(X), C.c_int64(N), D, _p(kr), len(kr), C.byref(opts), C.byref(best), _p(bic)))

@@ -56,7 +56,7 @@ class _Params(C.Structure):
 
 class _FitOpts(C.Structure):
     _fields_ = [("init", C.c_int32), ("tol", C.c_double), ("max_iter", C.c_int32), ("reg", C.c_double),
-                ("seed", C.c_uint64)]
+                ("seed", C.c_uint64), ("covariance_type", C.c_int32)]
 
 
 class _FitReport(C.Structure):
@@ -293,24 +293,25 @@ def _as_dataset(X, ctx: Optional[Context]) -> Dataset:
     return X if isinstance(X, Dataset) else Dataset.from_array(X, ctx)
 
 
-def _opts(init, tol, max_iter, reg, seed) -> _FitOpts:
+def _opts(init, tol, max_iter, reg, seed, covariance_type="full") -> _FitOpts:
     code = {"random": ES_INIT_RANDOM, "kmeans++": ES_INIT_KMEANSPP, "kmeanspp": ES_INIT_KMEANSPP,
             "given": ES_INIT_GIVEN}[init] if isinstance(init, str) else int(init)
     env = os.environ.get("EACGM_SEED")
     if env is not None:
         seed = int(env)
-    return _FitOpts(code, float(tol), int(max_iter), -1.0 if reg is None else float(reg), int(seed))
+    return _FitOpts(code, float(tol), int(max_iter), -1.0 if reg is None else float(reg), int(seed),
+                    {"full": 0, "diag": 1}[covariance_type])
 
 
 class EM:
     """Stepwise EM engine (es_gmm_em_begin/step/end): same semantics as fit_em."""
 
     def __init__(self, X, K: int, init="kmeans++", tol=1e-6, max_iter=200, reg=None, seed=0,
-                 init_params: Optional[GmmModel] = None, ctx: Optional[Context] = None):
+                 init_params: Optional[GmmModel] = None, ctx: Optional[Context] = None, covariance_type="full"):
         self.ds = _as_dataset(X, ctx)
         self.ctx = self.ds.ctx
         self.K = K
-        o = _opts("given" if init_params is not None else init, tol, max_iter, reg, seed)
+        o = _opts("given" if init_params is not None else init, tol, max_iter, reg, seed, covariance_type)
         self.max_iter = o.max_iter
         keep = None
         pp = None
@@ -354,9 +355,11 @@ class EM:
 
 
 def fit_em(X, K: int, init="kmeans++", tol: float = 1e-6, max_iter: int = 200, reg: Optional[float] = None,
-           seed: int = 0, init_params: Optional[GmmModel] = None, ctx: Optional[Context] = None) -> GmmModel:
-    """EM fit.  Defaults per SPEC.md:319-321."""
-    em = EM(X, K, init, tol, max_iter, reg, seed, init_params, ctx)
+           seed: int = 0, init_params: Optional[GmmModel] = None, ctx: Optional[Context] = None,
+           covariance_type: str = "full") -> GmmModel:
+    """EM fit.  Defaults per SPEC.md:319-321.  covariance_type "diag" is an
+    extension (diagonal covariances, not in the reference)."""
+    em = EM(X, K, init, tol, max_iter, reg, seed, init_params, ctx, covariance_type)
     try:
         em.step(max(max_iter, 0))
         return em.finish()
@@ -466,13 +469,13 @@ def calibrate_threshold(model: GmmModel, X_train, q: float, mode: str = "compone
 
 
 def select_k_bic(X, k_range: Sequence[int], init="kmeans++", tol=1e-6, max_iter=200, reg=None, seed=0,
-                 ctx: Optional[Context] = None):
+                 ctx: Optional[Context] = None, covariance_type: str = "full"):
     """(best_K, bic_values); failed K -> NaN."""
     ds = _as_dataset(X, ctx)
     kr = np.ascontiguousarray(list(k_range), np.int32)
     bic = np.empty(len(kr))
     best = C.c_int32()
-    o = _opts(init, tol, max_iter, reg, seed)
+    o = _opts(init, tol, max_iter, reg, seed, covariance_type)
     _check(ds.ctx._lib.es_gmm_select_k_bic(ds.ctx.handle, ds.handle, C.c_void_p(kr.ctypes.data),
                                            C.c_int32(len(kr)), C.byref(o), C.byref(best),
                                            C.c_void_p(bic.ctypes.data)))

@@ -868,6 +868,140 @@ void launch_score(const double* X, int64_t n, int64_t ld, int D, int K, const do
     ++ls.launches;
 }
 
+// ================================================== diagonal covariance
+// Extension (not in the reference: SPEC.md:332).  Team of
+// TS = next_pow2(K) lanes per event, lane k evaluates component k
+// (q = sum_a (x_a - mu_ka)^2 / sigma2_ka) and accumulates its 2D+1 statistics
+// about c_k = mu_k(old) in FP64 registers.  Statistics use the canonical
+// packed layout with only the diagonal of s2 populated (finalize in diag mode).
+template <int DM>
+__global__ void __launch_bounds__(kBlock) k_em_diag(const double* __restrict__ X, int64_t n, int64_t ld, int D, int K,
+                                                   const double* __restrict__ model, double* __restrict__ partial) {
+    extern __shared__ __align__(16) double sm[];
+    const int MS = DM + 1;
+    double* sMu = sm;                 // K * MS
+    double* sP = sMu + K * MS;        // K * MS  (precisions 1/sigma^2)
+    double* sC = sP + K * MS;         // 2K: logpi, lognorm
+    const int TS = next_pow2(K);
+    const int EPW = 32 / TS;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tl = lane % TS, slot = lane / TS;
+    const int k = tl;
+    const bool kact = k < K;
+    const int kk = kact ? k : 0;
+    ModelView mv{K, D, const_cast<double*>(model)};
+    for (int e = threadIdx.x; e < K * DM; e += blockDim.x) {
+        const int c = e / DM, j = e % DM;
+        sMu[c * MS + j] = j < D ? mv.mu()[c * D + j] : 0.0;
+        sP[c * MS + j] = j < D ? 1.0 / mv.cov()[(int64_t)c * D * D + j * D + j] : 0.0;
+    }
+    for (int c = threadIdx.x; c < K; c += blockDim.x) {
+        sC[2 * c] = mv.logpi()[c];
+        sC[2 * c + 1] = mv.lognorm()[c];
+    }
+    __syncthreads();
+    const double* muk = sMu + kk * MS;
+    const double* pk = sP + kk * MS;
+    const double logpi = kact ? sC[2 * kk] : -INFINITY;
+    const double lognorm = sC[2 * kk + 1];
+    constexpr int NA = 1 + 2 * DM;
+    double acc[NA];
+#pragma unroll
+    for (int j = 0; j < NA; ++j) acc[j] = 0.0;
+    double ll_acc = 0.0;
+    for (int64_t it = 0;; ++it) {
+        const int64_t wbase = ((it * gridDim.x + blockIdx.x) * 8 + warp) * EPW;
+        if (wbase >= n) break;
+        const int64_t i = wbase + slot;
+        const bool valid = i < n;
+        double d[DM];
+        double q = 0.0;
+#pragma unroll
+        for (int j = 0; j < DM; ++j) {
+            const double x = (valid && j < D) ? __ldg(X + (int64_t)j * ld + i) : 0.0;
+            d[j] = (j < D) ? x - muk[j] : 0.0;
+            q = fma(d[j] * d[j], pk[j], q);
+        }
+        const double ln = lognorm - 0.5 * q;
+        const double w = kact ? logpi + ln : -INFINITY;
+        const TeamLse r = team_lse<1>(w, kact ? ln : -INFINITY, k, TS);
+        const double g = (valid && kact) ? exp(w - r.ll) : 0.0;
+        if (valid && tl == 0) ll_acc += r.ll;
+        acc[0] += g;
+#pragma unroll
+        for (int j = 0; j < DM; ++j) {
+            const double gd = g * d[j];
+            acc[1 + j] += gd;
+            acc[1 + DM + j] = fma(gd, d[j], acc[1 + DM + j]);
+        }
+    }
+    // slots within the warp, then warps in order (fixed-order reduction)
+#pragma unroll
+    for (int j = 0; j < NA; ++j)
+        for (int off = TS; off < 32; off <<= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], off);
+    for (int off = TS; off < 32; off <<= 1) ll_acc += __shfl_xor_sync(0xffffffffu, ll_acc, off);
+    __syncthreads();
+    double* sRed = sm;  // reuse: 8 warps x TS lanes x NA
+    if (slot == 0) {
+#pragma unroll
+        for (int j = 0; j < NA; ++j) sRed[((int64_t)warp * TS + tl) * NA + j] = acc[j];
+    }
+    __shared__ double sLL[8];
+    if (lane == 0) sLL[warp] = ll_acc;
+    __syncthreads();
+    const int SK = stat_k(D), NE = K * SK;
+    double* myp = partial + (int64_t)blockIdx.x * (NE + 1);
+    for (int e = threadIdx.x; e < NE; e += blockDim.x) {
+        const int c = e / SK, rr = e % SK;
+        int j = -1;
+        if (rr <= D) {
+            j = rr;  // N, s1
+        } else {
+            int p2 = rr - 1 - D, a = 0;
+            while (p2 >= D - a) {
+                p2 -= D - a;
+                ++a;
+            }
+            if (p2 == 0) j = 1 + DM + a;  // diagonal entry (a, a)
+        }
+        double v = 0.0;
+        if (j >= 0)
+            for (int wv = 0; wv < 8; ++wv) v += sRed[((int64_t)wv * TS + c) * NA + j];
+        myp[e] = v;
+    }
+    if (threadIdx.x == 0) {
+        double v = 0.0;
+        for (int wv = 0; wv < 8; ++wv) v += sLL[wv];
+        myp[NE] = v;
+    }
+}
+
+void launch_em_diag(const double* X, int64_t n, int64_t ld, int D, int K, const double* model, double* partial,
+                    int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls) {
+    const int grid = num_sms * 2;
+    *nblk = grid;
+    const int TS = next_pow2(K);
+    auto smem_for = [&](int DM) {
+        const size_t a = (size_t)(2 * K * (DM + 1) + 2 * K) * sizeof(double);
+        const size_t b = (size_t)8 * TS * (1 + 2 * DM) * sizeof(double);
+        return a > b ? a : b;
+    };
+    if (D <= 8) {
+        static bool at = false;
+        if (!at) { allow_max_smem(k_em_diag<8>); at = true; }
+        k_em_diag<8><<<grid, kBlock, smem_for(8), s>>>(X, n, ld, D, K, model, partial);
+    } else if (D <= 16) {
+        static bool at = false;
+        if (!at) { allow_max_smem(k_em_diag<16>); at = true; }
+        k_em_diag<16><<<grid, kBlock, smem_for(16), s>>>(X, n, ld, D, K, model, partial);
+    } else {
+        static bool at = false;
+        if (!at) { allow_max_smem(k_em_diag<32>); at = true; }
+        k_em_diag<32><<<grid, kBlock, smem_for(32), s>>>(X, n, ld, D, K, model, partial);
+    }
+    ++ls.launches;
+}
+
 // ======================================================= finalize / derive
 // Warp-cooperative Cholesky + inverse of the D x D matrix in A (smem).
 // Writes L, W = L^-1 (smem) and returns logdet in lane 0; false if not PD.
@@ -991,7 +1125,7 @@ __global__ void k_finalize(const double* __restrict__ stats, int G, int D, int K
     __syncthreads();
     const double* Lold = mv.L() + (int64_t)k * D * D;
     const double* cold = mv.mu() + (int64_t)k * D;
-    if (whitened) {
+    if (whitened == 1) {
         for (int e = threadIdx.x; e < D * D; e += blockDim.x) {
             const int a = e / D, b = e % D;
             double v = 0.0;
@@ -1017,7 +1151,7 @@ __global__ void k_finalize(const double* __restrict__ stats, int G, int D, int K
         for (int e = threadIdx.x; e < D * D; e += blockDim.x) {
             const int a = e / D, b = e % D;
             if (a > b) continue;
-            const double v = sM[a * D + b] + (a == b ? reg : 0.0);
+            const double v = (whitened == 2 && a != b) ? 0.0 : sM[a * D + b] + (a == b ? reg : 0.0);
             sA[a * D + b] = v;
             sA[b * D + a] = v;
         }
@@ -1045,7 +1179,7 @@ __global__ void k_finalize(const double* __restrict__ stats, int G, int D, int K
     }
 }
 
-void launch_finalize(const double* stats, int G, int D, int K, int64_t n_global, double reg, bool whitened,
+void launch_finalize(const double* stats, int G, int D, int K, int64_t n_global, double reg, int whitened,
                      double* model, IterStatus* st, double* record, int t, cudaStream_t s, LaunchStats& ls) {
     const size_t smem = (size_t)(stat_k(D) + 5 * D * D + D) * sizeof(double);
     static bool attr = false;
@@ -1053,7 +1187,7 @@ void launch_finalize(const double* stats, int G, int D, int K, int64_t n_global,
         allow_max_smem(k_finalize);
         attr = true;
     }
-    k_finalize<<<K, 128, smem, s>>>(stats, G, D, K, n_global, reg, whitened ? 1 : 0, model, st, record, t);
+    k_finalize<<<K, 128, smem, s>>>(stats, G, D, K, n_global, reg, whitened, model, st, record, t);
     ++ls.launches;
 }
 

@@ -49,8 +49,12 @@ void launch_col_stats(const double* X, int64_t n, int64_t ld, int D, double* scr
                       cudaStream_t s, LaunchStats& ls);
 // M-step finalize from G rank blocks of statistics (summed in rank order),
 // updating the model in place and writing IterStatus (+ logL record[t]).
-void launch_finalize(const double* stats, int G, int D, int K, int64_t n_global, double reg, bool whitened,
+// whitened: 0 raw statistics, 1 whitened (team kernels), 2 raw + diagonal covariance
+void launch_finalize(const double* stats, int G, int D, int K, int64_t n_global, double reg, int whitened,
                      double* model, IterStatus* st, double* record, int t, cudaStream_t s, LaunchStats& ls);
+// Diagonal-covariance E+M pass (FP64 team kernel, D <= 32, K <= 32).
+void launch_em_diag(const double* X, int64_t n, int64_t ld, int D, int K, const double* model, double* partial,
+                    int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
 // Derive L, W, lognorm, logpi from pi, mu, cov in `model` (all components).
 void launch_derive(double* model, int D, int K, IterStatus* st, cudaStream_t s, LaunchStats& ls);
 // Scoring pass; `blocksum` receives per-CTA [ll_sum, flag_count] pairs.

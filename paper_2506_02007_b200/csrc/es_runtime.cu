@@ -518,6 +518,8 @@ double radix_select(es_ctx* c, const double* dkeys, int64_t n, int64_t r) {
 }
 
 // ---------------------------------------------------------------- EM core
+bool is_diag(const es_em_state* st) { return st->opts.covariance_type == ES_COV_DIAG; }
+
 void em_init_model(es_em_state* st, const es_gmm_params* init, const DataStats& dsx) {
     es_ctx* c = st->ctx;
     es_dataset* ds = st->ds;
@@ -602,7 +604,8 @@ void em_init_model(es_em_state* st, const es_gmm_params* init, const DataStats& 
             std::copy(&X0[(size_t)k * D], &X0[(size_t)k * D] + D, &mu[(size_t)k * D]);
             for (int a = 0; a < D; ++a)
                 for (int b = 0; b < D; ++b)
-                    cov[(size_t)k * D * D + a * D + b] = dsx.S[(size_t)a * D + b] + (a == b ? st->reg : 0.0);
+                    cov[(size_t)k * D * D + a * D + b] =
+                        (is_diag(st) && a != b) ? 0.0 : dsx.S[(size_t)a * D + b] + (a == b ? st->reg : 0.0);
         }
     }
     double* m = c->model.as<double>(mstride(K, D));
@@ -616,6 +619,10 @@ void em_begin(es_em_state* st, const es_gmm_params* init) {
     if (K < 1 || ds->n_global < K) fail(ES_ERR_DATA, "TooFewPoints", "fit_em requires N >= K >= 1");
     if (K > 128) fail(ES_ERR_DATA, "InvalidModel", "K must be <= 128");
     if (st->opts.max_iter < 0) fail(ES_ERR_DATA, "RangeViolation", "max_iter must be >= 0");
+    if (st->opts.covariance_type != ES_COV_FULL && st->opts.covariance_type != ES_COV_DIAG)
+        fail(ES_ERR_DATA, "RangeViolation", "covariance_type must be ES_COV_FULL or ES_COV_DIAG");
+    if (st->opts.covariance_type == ES_COV_DIAG && (K > 32 || D > 32))
+        fail(ES_ERR_DATA, "Unsupported", "diagonal covariance supports K <= 32, D <= 32");
     DataStats dsx = data_stats(c, ds);
     if (dsx.nonfinite > 0) fail(ES_ERR_DATA, "NonFiniteInput", "X contains non-finite entries");
     if (K > 1) {
@@ -642,11 +649,20 @@ bool em_iterate(es_em_state* st) {
     double* backup = c->model_backup.as<double>(mstride(K, D));
     CU(cudaMemcpyAsync(backup, dmodel, mstride(K, D) * 8, cudaMemcpyDeviceToDevice, c->stream));
     double* loc = c->stats_local.as<double>(NE1);
-    bool whitened = true;
-    if (ds->n_local > 0) {
+    int whitened = 1;
+    if (ds->n_local > 0 && is_diag(st)) {
+        int nblk = 0;
+        double* part = c->partial.as<double>((size_t)2 * c->num_sms * NE1);
+        c->t_begin();
+        launch_em_diag(ds->X, ds->n_local, ds->ld, D, K, dmodel, part, c->num_sms, &nblk, c->stream, c->ls);
+        c->t_end(c->em_ms, c->em_launches);
+        launch_reduce_blocks(part, nblk, NE1, loc, c->stream, c->ls);
+        whitened = 2;
+    } else if (ds->n_local > 0) {
         int nblk = 0;
         double* part = c->partial.as<double>((size_t)std::max(em_grid(D, K, c->num_sms), c->num_sms) * NE1);
         c->t_begin();
+        bool wh = true;
         if (c->precision == 0 && em_fast_supported(D, K)) {
             if (em_ws_enabled() && ds->has_xmap)
                 launch_em_ws(&ds->xmap, ds->n_local, D, K, dmodel, st->dcenter.as<double>(D), part, c->num_sms,
@@ -657,16 +673,19 @@ bool em_iterate(es_em_state* st) {
             else
                 launch_em_fast(ds->X, ds->n_local, ds->ld, D, K, dmodel, st->dcenter.as<double>(D), part,
                                c->num_sms, &nblk, c->stream, c->ls);
-            whitened = false;
+            wh = false;
         } else {
-            launch_em_pass(ds->X, ds->n_local, ds->ld, D, K, dmodel, part, c->num_sms, &nblk, &whitened, c->stream,
+            launch_em_pass(ds->X, ds->n_local, ds->ld, D, K, dmodel, part, c->num_sms, &nblk, &wh, c->stream,
                            c->ls);
         }
+        whitened = wh ? 1 : 0;
         c->t_end(c->em_ms, c->em_launches);
         launch_reduce_blocks(part, nblk, NE1, loc, c->stream, c->ls);
     } else {
         CU(cudaMemsetAsync(loc, 0, NE1 * 8, c->stream));
-        whitened = !(c->precision == 0 && em_fast_supported(D, K)) && em_path(D, K) != EmPath::Generic;
+        whitened = is_diag(st) ? 2
+                   : (!(c->precision == 0 && em_fast_supported(D, K)) && em_path(D, K) != EmPath::Generic) ? 1
+                                                                                                            : 0;
     }
     double* all = c->stats_all.as<double>((size_t)NE1 * c->world);
     c->allgather(loc, all, NE1);
@@ -710,7 +729,8 @@ bool em_iterate(es_em_state* st) {
             std::copy(row.begin(), row.end(), &mu[(size_t)k * D]);
             for (int a = 0; a < D; ++a)
                 for (int b = 0; b < D; ++b)
-                    cov[(size_t)k * D * D + a * D + b] = st->S[(size_t)a * D + b] + (a == b ? st->reg : 0.0);
+                    cov[(size_t)k * D * D + a * D + b] =
+                        (is_diag(st) && a != b) ? 0.0 : st->S[(size_t)a * D + b] + (a == b ? st->reg : 0.0);
             pi[k] = 1.0 / K;
         }
         double z = 0.0;
@@ -1255,7 +1275,9 @@ int es_gmm_select_k_bic(es_ctx* c, es_dataset* ds, const int32_t* k_range, int32
                 lm = g_msg;
                 continue;
             }
-            const double p = (K - 1) + (double)K * D + (double)K * D * (D + 1) / 2.0;
+            const double p = (K - 1) + (double)K * D +
+                             (opts->covariance_type == ES_COV_DIAG ? (double)K * D
+                                                                   : (double)K * D * (D + 1) / 2.0);
             bic[j] = -2.0 * rep.final_log_likelihood + p * std::log((double)ds->n_global);
             if (bic[j] < best_bic) {
                 best_bic = bic[j];

@@ -16,7 +16,7 @@ from sklearn.mixture import GaussianMixture
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def make(name, N, D, K, iters, seed):
+def make(name, N, D, K, iters, seed, covariance_type="full"):
     rng = np.random.default_rng(seed)
     centers = rng.uniform(-4, 4, size=(K, D))
     comp = rng.integers(0, K, size=N)
@@ -28,11 +28,18 @@ def make(name, N, D, K, iters, seed):
     w0 = np.full(K, 1.0 / K)
     mu0 = X[rows].copy()
     cov0 = np.repeat((S + reg * np.eye(D))[None], K, axis=0)
-    gm = GaussianMixture(n_components=K, covariance_type="full", tol=0.0, max_iter=iters, reg_covar=reg,
-                         weights_init=w0, means_init=mu0, precisions_init=np.linalg.inv(cov0), n_init=1)
+    if covariance_type == "diag":
+        cov0 = np.repeat(np.diag(np.diag(S) + reg)[None], K, axis=0)
+        prec0 = 1.0 / np.diagonal(cov0, axis1=1, axis2=2)
+    else:
+        prec0 = np.linalg.inv(cov0)
+    gm = GaussianMixture(n_components=K, covariance_type=covariance_type, tol=0.0, max_iter=iters, reg_covar=reg,
+                         weights_init=w0, means_init=mu0, precisions_init=prec0, n_init=1)
     gm.fit(X)
     np.savez_compressed(os.path.join(HERE, name), X=X, w0=w0, mu0=mu0, cov0=cov0, reg=reg, iters=iters,
-                        weights=gm.weights_, means=gm.means_, covariances=gm.covariances_,
+                        weights=gm.weights_, means=gm.means_,
+                        covariances=(np.array([np.diag(c) for c in gm.covariances_]) if covariance_type == "diag"
+                                     else gm.covariances_), covariance_type=covariance_type,
                         lower_bounds=np.array(gm.lower_bounds_), score=gm.score_samples(X),
                         predict=gm.predict(X), sklearn_version=sklearn.__version__)
 
@@ -40,4 +47,5 @@ def make(name, N, D, K, iters, seed):
 if __name__ == "__main__":
     make("sklearn_d3k3.npz", 3000, 3, 3, 25, 11)
     make("sklearn_d8k4.npz", 2000, 8, 4, 15, 12)
+    make("sklearn_diag_d6k5.npz", 3000, 6, 5, 20, 13, covariance_type="diag")
     print("ok")

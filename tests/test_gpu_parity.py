@@ -220,3 +220,18 @@ def test_layouts_and_generator(es, oracle):
     model = oracle.syn_model(42, 8, 4)
     Xo, _, _ = oracle.syn_rows(42, 8, 4, model, 0, 4096)
     assert np.abs(ds.read_rows() - Xo).max() < 1e-12 * max(1.0, np.abs(Xo).max())
+
+
+# ------------------------------------------------- diagonal covariance (a11)
+@pytest.mark.parametrize("D,K,n,iters", [(16, 16, 1 << 18, 15), (5, 3, 50_001, 30), (24, 8, 40_000, 8)])
+def test_diag_fit_parity(es, oracle, D, K, n, iters):
+    ds, X = syn(es, oracle, n, D, min(K, 8), seed=3)
+    m = es.fit_em(ds, K, init="random", tol=0.0, max_iter=iters, seed=5, covariance_type="diag")
+    pi, mu, cov, rep = oracle.fit_em(X, K, init="random", tol=0.0, max_iter=iters, seed=5, covariance_type="diag")
+    assert_params(m, pi, mu, cov)
+    off = m.covariances - np.array([np.diag(np.diag(c)) for c in m.covariances])
+    assert np.all(off == 0.0)
+    assert np.allclose(m.fit_report.per_iteration_log_likelihoods, rep["per_iteration_log_likelihoods"],
+                       rtol=LL_TOL)
+    best, bic = es.select_k_bic(ds, [K], init="random", max_iter=3, seed=5, covariance_type="diag")
+    assert best == K and np.isfinite(bic[0])

@@ -196,13 +196,14 @@ def test_calibrate_examples(oracle):
 
 
 # ------------------------------------------------------- sklearn fixtures
-@pytest.mark.parametrize("name", ["sklearn_d3k3.npz", "sklearn_d8k4.npz"])
+@pytest.mark.parametrize("name", ["sklearn_d3k3.npz", "sklearn_d8k4.npz", "sklearn_diag_d6k5.npz"])
 def test_oracle_matches_sklearn(oracle, name):
     g = np.load(os.path.join(GOLD, name))
     X = g["X"]
     iters = int(g["iters"])
+    ct = str(g["covariance_type"]) if "covariance_type" in g else "full"
     pi, mu, cov, rep = oracle.fit_em(X, len(g["w0"]), init_params=(g["w0"], g["mu0"], g["cov0"]), tol=0.0,
-                                     max_iter=iters, reg=float(g["reg"]))
+                                     max_iter=iters, reg=float(g["reg"]), covariance_type=ct)
     assert np.allclose(pi, g["weights"], rtol=1e-9, atol=1e-12)
     assert np.allclose(mu, g["means"], rtol=1e-9, atol=1e-9)
     assert np.allclose(cov, g["covariances"], rtol=1e-8, atol=1e-10)
