@@ -319,9 +319,9 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_ws(const __grid_constant__ CUten
                     for (int e0 = 0; e0 < nk; e0 += 32) {
                         const int e = e0 + lane;
                         const bool ve = e < nk;
-                        const int sw = (e >= p1) + (e >= p2) + (e >= p3);
-                        const int base = sw == 0 ? 0 : sw == 1 ? p1 : sw == 2 ? p2 : p3;
-                        const int ix = (kw * 4 + sw) * 32 + (e - base);
+                        // branch-free (sub-list, offset) of dense index e
+                        const int b1 = e >= p1, b2 = e >= p2, b3 = e >= p3;
+                        const int ix = (kw * 4 + b1 + b2 + b3) * 32 + e - (b1 * c0 + b2 * c1 + b3 * c2);
                         const int tt = ve ? R.lt[ix] : 0;
                         const float gg = ve ? R.lg[ix] : 0.f;
                         const float4* xr4 = reinterpret_cast<const float4*>(R.xr + tt * XR);
