@@ -1,0 +1,621 @@
+// es_em_mma.cu — fused EM pass with BOTH the E-step whitening and the M-step
+// Gram on the 5th-gen tensor cores (default for D <= 16, K <= 8).
+//
+// Per 128-event tile (one CTA per SM, persistent over tiles):
+//   converter WG  thread = event: coalesced loads of the FP64 planes (one tile of
+//                 prefetch in registers), x^ = (x - c) xs -> an FP32 row (for the
+//                 records) and the fp16 hi + lo K-major UMMA operand.
+//   MMA warp      E:  U = W' x^ + b'  as 4 kind::f16 dispatches (x_hi W_hi,
+//                     x_hi W_lo, x_lo W_hi, 1 * [b_hi b_lo]) -> TMEM, M = N = 128;
+//                 M:  Gram of the tile's per-event records over its 128 events
+//                     (8 K-steps of 16 events), M = 128 rows (k, a).
+//   epilogue WG   thread = event = TMEM lane: squared norms of U, log-sum-exp,
+//                 sqrt(responsibilities) s_k, the records; and thread = (k, a) =
+//                 TMEM lane of the Gram accumulator: the flush of the Gram of the
+//                 previous-but-one tile (double-buffered in TMEM, flushed every
+//                 tile), FP32 over <= 8 tiles, then FP64 in shared memory.
+//
+// Records (fp16, MN-major, one 19-group row per event):
+//   group 0: s_h/2 | groups 1..16: R_h = fp16(s_k (x^ - m_k)) | 17: s_h | 18: s_l
+//   and (NPASS = 2) a second record 2 R_l = fp16(2 (r - R_h)).
+// Pass 1:  R_h^T [R_h | s_h | s_l]     (N = 144; N = 136 without s_l)
+// Pass 2:  (2 R_l)^T R_h, (2 R_l)^T (s_h/2)   (N = 128 + 8)
+// so that P = R_h^T R_h + 2 R_l^T R_h and sym(P) = R_h^T R_h + R_l^T R_h + R_h^T R_l
+// (the Gram to ~2^-22), and the first moment R_h s_h + R_h s_l + R_l s_h.
+// NPASS = 1 keeps only R_h^T [R_h | s_h] (2^-12 per-event rounding noise).
+//
+// Numerics.  tcgen05 accumulates in FP32 with truncation
+// toward zero (measured ~1 ulp of the running sum per dispatch,
+// scripts/umma_probe.cu), so nothing that cancels is accumulated on the tensor
+// core: U only feeds the responsibilities, and the Gram is of records centred on
+// a per-CTA running estimate of the new mean (recentred after tiles 1, 2, 4, ...
+// with an exact FP64 re-expression; re-expressed about the starting centre at the
+// end), whose truncation bias is ~8 ulp of a same-sign per-tile sum (~6e-7).
+// xs is a power of two bringing max|x - c| into (8, 16]; t_k (a power of two)
+// puts the largest |entry| of W'/t_k, b'/t_k into (2^12, 2^13] so the fp16 lo
+// parts of all but negligible entries are normal numbers.
+#include <cmath>
+#include <cstdlib>
+#include <cuda_fp16.h>
+#include <cudaTypedefs.h>
+
+#include "es_kernels.h"
+#include "es_tc.cuh"
+
+namespace es {
+
+namespace {
+
+using namespace tc;
+
+constexpr int DM = 16, KMAX = 8, TM = 128;
+constexpr int NTHR = 320;              // WG0, WG1 (alternate tiles), warp 8 TMA, warp 9 MMA
+constexpr int XS = 2;                  // FP64 tile stages (TMA)
+constexpr uint32_t OPB = 4096;         // one 128 x 16 fp16 K-major operand
+constexpr uint32_t GRP = (TM / 8) * 128;   // one MN-major group of 8 columns: 16 K-groups x 128 B
+constexpr uint32_t RECH = 19 * GRP;        // 38912 B
+constexpr uint32_t RECL = 16 * GRP;        // 32768 B
+constexpr int MREG0 = 128, MREGS = 152;    // Gram regions at TMEM columns [128, 280) and [280, 432)
+
+// kind::f16 instruction descriptor: D = F32, A = B = F16, N>>3 @17, M>>4 @24,
+// transpose (MN-major) A @15, B @16.
+constexpr uint32_t idesc_f16(int M, int N, int mn) {
+    return (1u << 4) | ((uint32_t)mn << 15) | ((uint32_t)mn << 16) | ((uint32_t)(N >> 3) << 17) |
+           ((uint32_t)(M >> 4) << 24);
+}
+constexpr uint32_t kIdescE = idesc_f16(128, 128, 0);
+
+template <int NPASS>
+struct Smem {
+    double xd[XS][DM * TM];                             // 32 KB  FP64 tiles (planar, TMA destination)
+    unsigned char rech[2][RECH];                        // 76 KB  hi records (per warpgroup)
+    unsigned char recl[2][NPASS == 2 ? RECL : 16];      // 64 KB  2 x lo records
+    unsigned char ae[2][2][OPB];                        // 16 KB  x^ hi / lo (per warpgroup)
+    unsigned char aone[OPB];                            // ones in K columns 0, 1
+    unsigned char bw[2][OPB];                           // W' hi / lo
+    unsigned char bb[OPB];                              // b' hi, lo in K columns 0, 1
+    double c[DM];
+    double shift[2][KMAX * DM];                         // record centre - starting centre (FP64, exact)
+    double dl[2][KMAX * DM], s1x[2][KMAX * DM];         // recentring exchange
+    double wred[8][KMAX + 1];                           // per-warp partial N_k | logL
+    double ntot[2][KMAX];
+    float nmu[2][KMAX * DM];                            // -(record centre), x^ units, FP32
+    float cst[KMAX];                                    // log pi_k + lognorm_k
+    float hq[KMAX];                                     // 0.5 t_k^2
+    float tk[KMAX];
+    uint64_t xfull[XS], xfree[XS], aeready[2], edone[2], mready[2], mdone[2], efree;
+    uint32_t tmem;
+};
+
+// byte offset of (row, k) in a K-major 128 x 16 fp16 operand (SWIZZLE_NONE core matrices)
+__device__ __forceinline__ uint32_t kmaj(int row, int k) {
+    return (uint32_t)((row >> 3) * 256 + (k >> 3) * 128 + (row & 7) * 16 + (k & 7) * 2);
+}
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+}
+__device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count));
+}
+__device__ __forceinline__ void arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr)
+        : "memory");
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+}
+__device__ __forceinline__ void tmem_ld2(uint32_t taddr, float& a, float& b) {
+    uint32_t r0, r1;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(taddr) : "memory");
+    a = __uint_as_float(r0);
+    b = __uint_as_float(r1);
+}
+__device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
+__device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+// round-to-nearest, saturating fp32 pair -> fp16x2 (lo in the low half)
+__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+}  // namespace
+
+template <int NPASS>
+__global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUtensorMap xmap, int64_t n, int D,
+                                                     int K, const double* __restrict__ model,
+                                                     const double* __restrict__ center, double xs,
+                                                     double* __restrict__ partial) {
+    using Sm = Smem<NPASS>;
+    extern __shared__ __align__(128) unsigned char smraw[];
+    // keep the shared-window provenance of the pointer (generic LD/ST otherwise)
+    Sm& S = *reinterpret_cast<Sm*>(smraw + ((128u - (su32(smraw) & 127u)) & 127u));
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    ModelView mv{K, D, const_cast<double*>(model)};
+    const int64_t ntiles = (n + TM - 1) / TM;
+    const int64_t J = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+    // ------------------------------------------------------------------ staging
+    for (int j = t; j < DM; j += NTHR) S.c[j] = j < D ? center[j] : 0.0;
+    for (int e = t; e < XS * DM * TM; e += NTHR) (&S.xd[0][0])[e] = 0.0;  // planes >= D stay zero
+    if (t < KMAX) {
+        const int k = t;
+        float cst = -INFINITY, tkv = 1.f;
+        if (k < K) {
+            cst = (float)(mv.logpi()[k] + mv.lognorm()[k]);
+            double m = 0.0;
+            const double* W = mv.W() + (int64_t)k * D * D;
+            for (int a = 0; a < D; ++a) {
+                double b = 0.0;
+                for (int f = 0; f <= a; ++f) {
+                    m = fmax(m, fabs(W[a * D + f] / xs));
+                    b = fma(W[a * D + f], mv.mu()[k * D + f] - center[f], b);
+                }
+                m = fmax(m, fabs(b));
+            }
+            if (m > 0.0) tkv = (float)exp2(ceil(log2(m)) - 13.0);
+        }
+        S.cst[k] = cst;
+        S.hq[k] = 0.5f * tkv * tkv;
+        S.tk[k] = tkv;
+    }
+    for (int e = t; e < KMAX * DM; e += NTHR) {
+        const int k = e / DM, f = e % DM;
+        const float m0 = (k < K && f < D) ? -(float)((mv.mu()[k * D + f] - center[f]) * xs) : 0.f;
+        S.nmu[0][e] = S.nmu[1][e] = m0;
+        S.shift[0][e] = S.shift[1][e] = 0.0;
+    }
+    __syncthreads();
+    for (int e = t; e < TM * DM; e += NTHR) {
+        const int row = e / DM, f = e % DM, k = row / DM, a = row % DM;
+        double w = 0.0, b = 0.0;
+        if (k < K && a < D) {
+            const double* Wr = mv.W() + (int64_t)k * D * D + (int64_t)a * D;
+            const double inv_t = 1.0 / (double)S.tk[k];
+            if (f <= a) w = Wr[f] / xs * inv_t;
+            if (f < 2) {
+                double s = 0.0;
+                for (int q = 0; q <= a; ++q) s = fma(Wr[q], mv.mu()[k * D + q] - S.c[q], s);
+                b = -s * inv_t;
+            }
+        }
+        const __half wh = __double2half(w);
+        const __half wl = __double2half(w - (double)__half2float(wh));
+        *reinterpret_cast<__half*>(S.bw[0] + kmaj(row, f)) = wh;
+        *reinterpret_cast<__half*>(S.bw[1] + kmaj(row, f)) = wl;
+        const __half bh = __double2half(b);
+        const __half bl = __double2half(b - (double)__half2float(bh));
+        *reinterpret_cast<__half*>(S.bb + kmaj(row, f)) = f == 0 ? bh : (f == 1 ? bl : __half(0.f));
+        *reinterpret_cast<__half*>(S.aone + kmaj(row, f)) = __half(f < 2 ? 1.f : 0.f);
+    }
+    if (warp == 9) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&S.tmem)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (t == 0) {
+        for (int i = 0; i < XS; ++i) {
+            mbar_init(&S.xfull[i], 1);
+            mbar_init(&S.xfree[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&S.aeready[i], 1);
+            mbar_init(&S.edone[i], 1);
+            mbar_init(&S.mready[i], 4);
+            mbar_init(&S.mdone[i], 1);
+        }
+        mbar_init(&S.efree, 4);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    proxy_fence();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = S.tmem;
+    auto tile_of = [&](int64_t j) { return (int64_t)blockIdx.x + j * gridDim.x; };
+
+    if (warp < 8) {
+        // ====================================================== epilogue warpgroups
+        // WG w takes tiles j = w, w + 2, ...: converts its FP64 tile, then (thread =
+        // event = TMEM lane) reads U, forms the responsibilities and the records; as
+        // thread = (k, a) it flushes its own Gram region.
+        const int w = warp >> 2;
+        const int p = t & 127;             // event row of the tile / Gram row (k, a)
+        const int q = warp & 3;            // TMEM lane quadrant
+        const uint32_t lq = (uint32_t)(32 * q) << 16;
+        const int hsel = lane >> 4;        // Gram row (k, a): k = 2q + hsel, a = lane & 15
+        const int kk = p >> 4, aa = p & 15;
+        float cst[KMAX], hq[KMAX];
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) {
+            cst[k] = S.cst[k];
+            hq[k] = S.hq[k];
+        }
+        double g2[DM], g1 = 0.0, nk[KMAX], llacc = 0.0;
+#pragma unroll
+        for (int b = 0; b < DM; ++b) g2[b] = 0.0;
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) nk[k] = 0.0;
+
+        auto flush = [&](int64_t jj) {  // Gram of this WG's local tile jj -> FP64
+            mbar_wait(su32(&S.mdone[w]), (uint32_t)(jj & 1));
+            tc_fence_after();
+            const uint32_t rg = (uint32_t)(MREG0 + MREGS * w), xg = rg + 8;
+            float v[32], f0, f1, m1;
+            tmem_ld32(tmem + lq + xg + 32 * q, v);
+            tmem_ld2(tmem + lq + xg + TM + 2 * q, f0, f1);
+            if (NPASS == 2) {
+                float e0, e1, c0, c1;
+                tmem_ld2(tmem + lq + xg + TM + KMAX + 2 * q, e0, e1);
+                tmem_ld2(tmem + lq + rg + 2 * q, c0, c1);
+                tmem_wait_ld();
+                m1 = hsel ? f1 + (e1 + c1) : f0 + (e0 + c0);
+            } else {
+                tmem_wait_ld();
+                m1 = hsel ? f1 : f0;
+            }
+#pragma unroll
+            for (int b = 0; b < DM; ++b) g2[b] += (double)(hsel ? v[16 + b] : v[b]);
+            g1 += (double)m1;
+            tc_fence_before();
+        };
+        // N_k of this WG (fixed-order reduction) -> S.ntot[w]
+        auto wg_counts = [&]() {
+#pragma unroll
+            for (int k = 0; k < KMAX; ++k) {
+                const double v = warp_sum(nk[k]);
+                if (lane == 0) S.wred[warp][k] = v;
+            }
+            named_sync(3 + w, 128);
+            if (p < KMAX) {
+                double s = 0.0;
+                for (int i = 0; i < 4; ++i) s += S.wred[4 * w + i][p];
+                S.ntot[w][p] = s;
+            }
+            named_sync(3 + w, 128);
+        };
+        // Move this WG's accumulation centre for component k to its running estimate of
+        // the new mean (x^ units, rounded to FP32 for the records) and re-express the
+        // FP64 statistics about it exactly:
+        //   P' = P - s1 d^T - d s1^T + N d d^T,  s1' = s1 - N d.
+        // `back` re-expresses about the kernel's starting centre instead (d = -shift).
+        auto recentre = [&](bool back) {
+            wg_counts();
+            const double N = S.ntot[w][kk];
+            double d = 0.0;
+            if (back) {
+                d = -S.shift[w][p];
+            } else if (kk < K && aa < D && N > 0.5) {
+                const float cur = -S.nmu[w][p];
+                const float nw = (float)((double)cur + g1 / N);
+                d = (double)nw - (double)cur;
+            }
+            S.dl[w][p] = d;
+            S.s1x[w][p] = g1;
+            named_sync(3 + w, 128);
+#pragma unroll
+            for (int bb = 0; bb < DM; ++bb) {
+                const double db = S.dl[w][kk * DM + bb], sb = S.s1x[w][kk * DM + bb];
+                g2[bb] += fma(N * d, db, -fma(g1, db, d * sb));
+            }
+            g1 = fma(-N, d, g1);
+            if (!back) {
+                S.nmu[w][p] = -(float)(-(double)S.nmu[w][p] + d);
+                S.shift[w][p] += d;
+            }
+            named_sync(3 + w, 128);
+        };
+
+        bool pend = false;   // the Gram of this WG's previous tile is still to be flushed
+        int64_t jj = 0;      // local tile index
+        for (int64_t j = w; j < J; j += 2, ++jj) {
+            const int s = (int)(j % XS);
+            const bool valid = tile_of(j) * TM + p < n;
+            // ---- convert: x^ = (x - c) xs -> FP32 row (registers) + fp16 hi/lo operand
+            mbar_wait(su32(&S.xfull[s]), (uint32_t)((j / XS) & 1));
+            uint64_t x2[DM / 2];
+            {
+                uint32_t hw[DM / 2], lw[DM / 2];
+#pragma unroll
+                for (int f = 0; f < DM; f += 2) {
+                    const float v0 = (float)((S.xd[s][f * TM + p] - S.c[f]) * xs);
+                    const float v1 = (float)((S.xd[s][(f + 1) * TM + p] - S.c[f + 1]) * xs);
+                    x2[f / 2] = pack2(v0, v1);
+                    const uint32_t h = pack_h2(v0, v1);
+                    const float2 hf = __half22float2(u2h(h));
+                    hw[f / 2] = h;
+                    lw[f / 2] = pack_h2(v0 - hf.x, v1 - hf.y);
+                }
+#pragma unroll
+                for (int g = 0; g < 2; ++g) {
+                    *reinterpret_cast<uint4*>(S.ae[w][0] + kmaj(p, 8 * g)) =
+                        make_uint4(hw[4 * g], hw[4 * g + 1], hw[4 * g + 2], hw[4 * g + 3]);
+                    *reinterpret_cast<uint4*>(S.ae[w][1] + kmaj(p, 8 * g)) =
+                        make_uint4(lw[4 * g], lw[4 * g + 1], lw[4 * g + 2], lw[4 * g + 3]);
+                }
+            }
+            proxy_fence();
+            named_sync(1 + w, 128);
+            if (p == 0) {
+                arrive(&S.xfree[s]);
+                arrive(&S.aeready[w]);
+            }
+            // ---- E-step epilogue
+            mbar_wait(su32(&S.edone[w]), (uint32_t)(jj & 1));
+            tc_fence_after();
+            float wk[KMAX];
+            float mx = -INFINITY;
+#pragma unroll
+            for (int k = 0; k < KMAX; ++k) {
+                float u[16];
+                tmem_ld16(tmem + lq + 16 * k, u);
+                tmem_wait_ld();
+                uint64_t q2 = 0;
+#pragma unroll
+                for (int r = 0; r < 16; r += 2) {
+                    const uint64_t uu = pack2(u[r], u[r + 1]);
+                    ffma2(q2, uu, uu);
+                }
+                float qa, qb;
+                unpack2(q2, qa, qb);
+                wk[k] = cst[k] - hq[k] * (qa + qb);
+                mx = fmaxf(mx, wk[k]);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) arrive(&S.efree);
+            float ssum = 0.f;
+#pragma unroll
+            for (int k = 0; k < KMAX; ++k) ssum += exp2f((wk[k] - mx) * 1.4426950408889634f);
+            const float ll = mx + log2f(ssum) * 0.6931471805599453f;
+            float sg[KMAX];
+#pragma unroll
+            for (int k = 0; k < KMAX; ++k) {
+                sg[k] = valid ? exp2f((wk[k] - ll) * 0.7213475204444817f) : 0.f;
+                nk[k] += (double)(sg[k] * sg[k]);
+            }
+            if (valid) llacc += (double)ll;
+            // ---- records (buffers w are free once the Gram of the previous tile completed)
+            if (pend) {
+                flush(jj - 1);
+                pend = false;
+            }
+            unsigned char* rh = S.rech[w] + (p >> 3) * 128 + (p & 7) * 16;
+            unsigned char* rl = S.recl[w] + (p >> 3) * 128 + (p & 7) * 16;
+#pragma unroll
+            for (int k = 0; k < KMAX; ++k) {
+                const uint64_t s2 = pack2(sg[k], sg[k]);
+                const ulonglong2* nm = reinterpret_cast<const ulonglong2*>(S.nmu[w] + k * DM);
+                uint32_t oh[8], ol[8];
+#pragma unroll
+                for (int r = 0; r < 8; r += 2) {
+                    const ulonglong2 m2 = nm[r / 2];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const uint64_t rr = mul2(add2(x2[r + h], h ? m2.y : m2.x), s2);
+                        float lo, hi;
+                        unpack2(rr, lo, hi);
+                        oh[r + h] = pack_h2(lo, hi);
+                        if (NPASS == 2) {
+                            const float2 hf = __half22float2(u2h(oh[r + h]));
+                            const uint64_t dd = add2(rr, pack2(-hf.x, -hf.y));
+                            unpack2(add2(dd, dd), lo, hi);
+                            ol[r + h] = pack_h2(lo, hi);
+                        }
+                    }
+                }
+                *reinterpret_cast<uint4*>(rh + (1 + 2 * k) * GRP) = make_uint4(oh[0], oh[1], oh[2], oh[3]);
+                *reinterpret_cast<uint4*>(rh + (2 + 2 * k) * GRP) = make_uint4(oh[4], oh[5], oh[6], oh[7]);
+                if (NPASS == 2) {
+                    *reinterpret_cast<uint4*>(rl + (2 * k) * GRP) = make_uint4(ol[0], ol[1], ol[2], ol[3]);
+                    *reinterpret_cast<uint4*>(rl + (2 * k + 1) * GRP) = make_uint4(ol[4], ol[5], ol[6], ol[7]);
+                }
+            }
+            {
+                uint32_t sh[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) sh[r] = pack_h2(sg[2 * r], sg[2 * r + 1]);
+                *reinterpret_cast<uint4*>(rh + 17 * GRP) = make_uint4(sh[0], sh[1], sh[2], sh[3]);
+                if (NPASS == 2) {
+                    uint32_t sl[4], s5[4];
+                    const __half2 half2_05 = __float2half2_rn(0.5f);
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const float2 hf = __half22float2(u2h(sh[r]));
+                        sl[r] = pack_h2(sg[2 * r] - hf.x, sg[2 * r + 1] - hf.y);
+                        s5[r] = h2u(__hmul2(u2h(sh[r]), half2_05));
+                    }
+                    *reinterpret_cast<uint4*>(rh + 18 * GRP) = make_uint4(sl[0], sl[1], sl[2], sl[3]);
+                    *reinterpret_cast<uint4*>(rh) = make_uint4(s5[0], s5[1], s5[2], s5[3]);
+                }
+            }
+            proxy_fence();
+            __syncwarp();
+            if (lane == 0) arrive(&S.mready[w]);
+            pend = true;
+            // recentre after local tiles 1, 2, 4, 8, ... (drain this WG's Gram first)
+            if (((jj + 1) & jj) == 0 && j + 2 < J) {
+                flush(jj);
+                pend = false;
+                recentre(false);
+            }
+        }
+        if (pend) flush(jj - 1);
+        recentre(true);
+        // -------------------------------------------------------------- output
+        // Sum the two WGs' statistics (fixed order) about the starting centre
+        // c + mu^_k / xs (x units; scale by xs^-1, xs^-2, exact) and symmetrise the
+        // Gram, sym(P) = (P + P^T) / 2.  The record buffers are free now (scratch).
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) {
+            const double v = warp_sum(nk[k]);
+            if (lane == 0) S.wred[warp][k] = v;
+        }
+        {
+            const double v = warp_sum(llacc);
+            if (lane == 0) S.wred[warp][KMAX] = v;
+        }
+        double* rows = reinterpret_cast<double*>(&S.rech[0][0]);  // [2][128][17]
+        named_sync(5, 256);  // both WGs drained: no Gram still reads the record buffers
+#pragma unroll
+        for (int b = 0; b < DM; ++b) rows[(w * TM + p) * (DM + 1) + b] = g2[b];
+        rows[(w * TM + p) * (DM + 1) + DM] = g1;
+        named_sync(5, 256);
+        if (w == 0) {
+            const int SK = stat_k(D), NE = K * SK;
+            double* myp = partial + (int64_t)blockIdx.x * (NE + 1);
+            const double i1 = 1.0 / xs, i2 = i1 * i1;
+            if (kk < K && aa < D) {
+                double* blk = myp + kk * SK;
+                const double* r0 = rows + p * (DM + 1);
+                const double* r1 = rows + (TM + p) * (DM + 1);
+                blk[1 + aa] = (r0[DM] + r1[DM]) * i1;
+                for (int bb = aa; bb < D; ++bb) {
+                    const double* c0 = rows + (kk * DM + bb) * (DM + 1);
+                    const double* c1 = rows + (TM + kk * DM + bb) * (DM + 1);
+                    blk[1 + D + packed_index(aa, bb, D)] = 0.5 * ((r0[bb] + r1[bb]) + (c0[aa] + c1[aa])) * i2;
+                }
+            }
+            if (p < K) {
+                double s = 0.0;
+                for (int i = 0; i < 8; ++i) s += S.wred[i][p];
+                myp[p * SK] = s;
+            }
+            if (p == KMAX) {
+                double s = 0.0;
+                for (int i = 0; i < 8; ++i) s += S.wred[i][KMAX];
+                myp[NE] = s;
+            }
+        }
+    } else if (warp == 8) {
+        // ========================================================== TMA producer
+        if (lane == 0) {
+            for (int64_t j = 0; j < J; ++j) {
+                const int s = (int)(j % XS);
+                if (j >= XS) mbar_wait_sleep(su32(&S.xfree[s]), (uint32_t)(((j - XS) / XS) & 1));
+                mbar_expect_tx(su32(&S.xfull[s]), (uint32_t)(D * TM * 8));
+                tma_load_2d(su32(&S.xd[s][0]), &xmap, (int)(tile_of(j) * TM), 0, su32(&S.xfull[s]));
+            }
+        }
+    } else {
+        // ========================================================== MMA issuer
+        if (lane == 0) {
+            const uint64_t dbh = sdesc(su32(S.bw[0]), 128, 256), dbl = sdesc(su32(S.bw[1]), 128, 256);
+            const uint64_t dbb = sdesc(su32(S.bb), 128, 256), done = sdesc(su32(S.aone), 128, 256);
+            constexpr uint32_t idesc1 = idesc_f16(128, NPASS == 2 ? 144 : 136, 1);
+            constexpr uint32_t idesc2a = idesc_f16(128, 128, 1);
+            constexpr uint32_t idesc2b = idesc_f16(128, 8, 1);
+            auto gram = [&](int64_t m) {
+                const int mw = (int)(m & 1);
+                mbar_wait_sleep(su32(&S.mready[mw]), (uint32_t)((m >> 1) & 1));
+                tc_fence_after();
+                const uint32_t rg = tmem + (uint32_t)(MREG0 + MREGS * mw), xg = rg + 8;
+                const uint32_t h0 = su32(S.rech[mw]), l0 = su32(S.recl[mw]);
+#pragma unroll
+                for (int ks = 0; ks < TM / 16; ++ks) {
+                    const uint64_t dh = sdesc(h0 + GRP + ks * 256, 128, GRP);  // groups 1.. (R_h, s_h, s_l)
+                    mma_f16(xg, dh, dh, idesc1, ks > 0 ? 1u : 0u);
+                    if (NPASS == 2) {
+                        const uint64_t dl = sdesc(l0 + ks * 256, 128, GRP);
+                        mma_f16(xg, dl, dh, idesc2a, 1u);
+                        mma_f16(rg, dl, sdesc(h0 + ks * 256, 128, GRP), idesc2b, ks > 0 ? 1u : 0u);
+                    }
+                }
+                commit(&S.mdone[mw]);
+            };
+            for (int64_t j = 0; j < J; ++j) {
+                const int w = (int)(j & 1);
+                mbar_wait_sleep(su32(&S.aeready[w]), (uint32_t)((j >> 1) & 1));
+                if (j >= 1) mbar_wait_sleep(su32(&S.efree), (uint32_t)((j - 1) & 1));
+                tc_fence_after();
+                const uint64_t dah = sdesc(su32(S.ae[w][0]), 128, 256), dal = sdesc(su32(S.ae[w][1]), 128, 256);
+                mma_f16(tmem, dah, dbh, kIdescE, 0u);
+                mma_f16(tmem, dah, dbl, kIdescE, 1u);
+                mma_f16(tmem, dal, dbh, kIdescE, 1u);
+                mma_f16(tmem, done, dbb, kIdescE, 1u);
+                commit(&S.edone[w]);
+                if (j >= 1) gram(j - 1);
+            }
+            if (J >= 1) gram(J - 1);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 9) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+bool em_mma_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ES_EM_KERNEL");
+        v = (!e || e[0] == 'm') ? 1 : 0;  // default; "ws" / "tc" / "simt" select the older kernels
+    }
+    return v == 1;
+}
+
+int em_mma_passes() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ES_EM_MMA_PASSES");
+        v = (e && e[0] == '1') ? 1 : 2;
+    }
+    return v;
+}
+
+template <int NPASS>
+static void launch_npass(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model,
+                         const double* center, double xs, double* partial, int grid, cudaStream_t s) {
+    const size_t smem = sizeof(Smem<NPASS>) + 128;
+    static bool a = false;
+    if (!a) {
+        cudaFuncSetAttribute(k_em_mma<NPASS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        a = true;
+    }
+    k_em_mma<NPASS><<<grid, NTHR, smem, s>>>(*xmap, n, D, K, model, center, xs, partial);
+}
+
+void launch_em_mma(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model, const double* center,
+                   double xs, double* partial, int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls) {
+    const int64_t ntiles = (n + TM - 1) / TM;
+    const int grid = (int)std::min<int64_t>(num_sms, std::max<int64_t>(ntiles, 1));
+    *nblk = grid;
+    if (em_mma_passes() == 1)
+        launch_npass<1>(xmap, n, D, K, model, center, xs, partial, grid, s);
+    else
+        launch_npass<2>(xmap, n, D, K, model, center, xs, partial, grid, s);
+    ++ls.launches;
+}
+
+}  // namespace es

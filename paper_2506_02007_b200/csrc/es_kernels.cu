@@ -1080,8 +1080,11 @@ void launch_derive(double* model, int D, int K, IterStatus* st, cudaStream_t s, 
 // M-step from the shifted statistics about c_k = mu_k(old):
 //   mu_new = c + T zbar,  Sigma_new = T (S2/N_k - zbar zbar^T) T^T + reg I
 // with T = L_k (whitened statistics) or I (raw), zbar = s1 / N_k.
+// whitened == 3: raw statistics about the centre c + fp32((mu_k - c) xs) / xs
+// (k_em_mma's record centre), given `center` = c and `xs`.
 __global__ void k_finalize(const double* __restrict__ stats, int G, int D, int K, int64_t n_global, double reg,
-                           int whitened, double* model, IterStatus* st, double* record, int t) {
+                           int whitened, double* model, IterStatus* st, double* record, int t,
+                           const double* __restrict__ center, double xs) {
     extern __shared__ double sm[];
     const int k = blockIdx.x;
     const int SK = stat_k(D), NE = K * SK, P = packed_size(D);
@@ -1155,7 +1158,11 @@ __global__ void k_finalize(const double* __restrict__ stats, int G, int D, int K
             sA[a * D + b] = v;
             sA[b * D + a] = v;
         }
-        for (int a = threadIdx.x; a < D; a += blockDim.x) sMu[a] = cold[a] + s1[a] * inv;
+        for (int a = threadIdx.x; a < D; a += blockDim.x) {
+            double c0 = cold[a];
+            if (whitened == 3) c0 = center[a] + (double)(float)((cold[a] - center[a]) * xs) / xs;
+            sMu[a] = c0 + s1[a] * inv;
+        }
     }
     __syncthreads();
     // write pi, mu, cov then derive L, W, lognorm, logpi
@@ -1180,14 +1187,15 @@ __global__ void k_finalize(const double* __restrict__ stats, int G, int D, int K
 }
 
 void launch_finalize(const double* stats, int G, int D, int K, int64_t n_global, double reg, int whitened,
-                     double* model, IterStatus* st, double* record, int t, cudaStream_t s, LaunchStats& ls) {
+                     double* model, IterStatus* st, double* record, int t, cudaStream_t s, LaunchStats& ls,
+                     const double* center, double xs) {
     const size_t smem = (size_t)(stat_k(D) + 5 * D * D + D) * sizeof(double);
     static bool attr = false;
     if (!attr) {
         allow_max_smem(k_finalize);
         attr = true;
     }
-    k_finalize<<<K, 128, smem, s>>>(stats, G, D, K, n_global, reg, whitened, model, st, record, t);
+    k_finalize<<<K, 128, smem, s>>>(stats, G, D, K, n_global, reg, whitened, model, st, record, t, center, xs);
     ++ls.launches;
 }
 

@@ -50,8 +50,10 @@ void launch_col_stats(const double* X, int64_t n, int64_t ld, int D, double* scr
 // M-step finalize from G rank blocks of statistics (summed in rank order),
 // updating the model in place and writing IterStatus (+ logL record[t]).
 // whitened: 0 raw statistics, 1 whitened (team kernels), 2 raw + diagonal covariance
+// whitened 3: raw statistics about c + fp32((mu_k - c) xs) / xs (k_em_mma), needs center and xs.
 void launch_finalize(const double* stats, int G, int D, int K, int64_t n_global, double reg, int whitened,
-                     double* model, IterStatus* st, double* record, int t, cudaStream_t s, LaunchStats& ls);
+                     double* model, IterStatus* st, double* record, int t, cudaStream_t s, LaunchStats& ls,
+                     const double* center = nullptr, double xs = 1.0);
 // Diagonal-covariance E+M pass (FP64 team kernel, D <= 32, K <= 32).
 void launch_em_diag(const double* X, int64_t n, int64_t ld, int D, int K, const double* model, double* partial,
                     int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
@@ -91,6 +93,12 @@ bool em_ws_enabled();
 // xmap: 2-D TMA tensor map over the planar event matrix (box = 128 rows x D planes).
 void launch_em_ws(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model, const double* center,
                   double* partial, int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
+// Fused pass with E-step and M-step Gram on tcgen05 (es_em_mma.cu), the default
+// for D <= 16, K <= 8 (ES_EM_KERNEL=mma|ws|tc|simt).  Writes finalize mode-3 statistics.
+bool em_mma_enabled();
+int em_mma_passes();  // 2 (hi + lo records, default) or 1 (ES_EM_MMA_PASSES=1)
+void launch_em_mma(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model, const double* center,
+                   double xs, double* partial, int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
 // Builds that tensor map (driver entry point resolved through the runtime).
 bool make_event_tmap(CUtensorMap* map, const double* X, int64_t n, int64_t ld, int D);
 // tcgen05 scoring pass (es_score_tc.cu); ES_SCORE_KERNEL=simt selects k_score_fast.

@@ -271,6 +271,7 @@ struct es_em_state {
     double reg = 0.0;
     std::vector<double> S;  // data covariance (D x D)
     std::vector<double> mean;  // data mean: FP64 centre of the mixed-precision path
+    double xs = 1.0;           // power of two bringing max|x - mean| into (8, 16] (k_em_mma operand scale)
     DevBuf dcenter;
     SplitMix64 rng{0};
     std::vector<double> per_iter;
@@ -633,6 +634,11 @@ void em_begin(es_em_state* st, const es_gmm_params* init) {
     }
     st->S = dsx.S;
     st->mean = dsx.mean;
+    {
+        double span = 0.0;
+        for (int j = 0; j < D; ++j) span = std::max(span, std::max(dsx.mx[j] - dsx.mean[j], dsx.mean[j] - dsx.mn[j]));
+        st->xs = span > 0.0 ? std::ldexp(1.0, 4 - (int)std::ceil(std::log2(span))) : 1.0;
+    }
     CU(cudaMemcpyAsync(st->dcenter.as<double>(D), dsx.mean.data(), D * 8, cudaMemcpyHostToDevice, c->stream));
     st->reg = st->opts.reg < 0 ? default_reg(dsx.S, D) : st->opts.reg;
     st->rng = SplitMix64(st->opts.seed);
@@ -662,9 +668,13 @@ bool em_iterate(es_em_state* st) {
         int nblk = 0;
         double* part = c->partial.as<double>((size_t)std::max(em_grid(D, K, c->num_sms), c->num_sms) * NE1);
         c->t_begin();
-        bool wh = true;
+        bool wh = true, wh_mma = false;
         if (c->precision == 0 && em_fast_supported(D, K)) {
-            if (em_ws_enabled() && ds->has_xmap)
+            if (em_mma_enabled() && ds->has_xmap) {
+                launch_em_mma(&ds->xmap, ds->n_local, D, K, dmodel, st->dcenter.as<double>(D), st->xs, part,
+                              c->num_sms, &nblk, c->stream, c->ls);
+                wh_mma = true;
+            } else if (em_ws_enabled() && ds->has_xmap)
                 launch_em_ws(&ds->xmap, ds->n_local, D, K, dmodel, st->dcenter.as<double>(D), part, c->num_sms,
                              &nblk, c->stream, c->ls);
             else if (em_tc_enabled())
@@ -678,21 +688,25 @@ bool em_iterate(es_em_state* st) {
             launch_em_pass(ds->X, ds->n_local, ds->ld, D, K, dmodel, part, c->num_sms, &nblk, &wh, c->stream,
                            c->ls);
         }
-        whitened = wh ? 1 : 0;
+        whitened = wh_mma ? 3 : (wh ? 1 : 0);
         c->t_end(c->em_ms, c->em_launches);
         launch_reduce_blocks(part, nblk, NE1, loc, c->stream, c->ls);
     } else {
         CU(cudaMemsetAsync(loc, 0, NE1 * 8, c->stream));
-        whitened = is_diag(st) ? 2
-                   : (!(c->precision == 0 && em_fast_supported(D, K)) && em_path(D, K) != EmPath::Generic) ? 1
-                                                                                                            : 0;
+        // an empty shard must announce the same statistics format as the others
+        if (is_diag(st))
+            whitened = 2;
+        else if (c->precision == 0 && em_fast_supported(D, K))
+            whitened = em_mma_enabled() ? 3 : 0;
+        else
+            whitened = em_path(D, K) != EmPath::Generic ? 1 : 0;
     }
     double* all = c->stats_all.as<double>((size_t)NE1 * c->world);
     c->allgather(loc, all, NE1);
     IterStatus* dst = c->status.as<IterStatus>(1);
     CU(cudaMemsetAsync(dst, 0, sizeof(IterStatus), c->stream));
     launch_finalize(all, c->world, D, K, ds->n_global, st->reg, whitened, dmodel, dst, nullptr, st->t, c->stream,
-                    c->ls);
+                    c->ls, st->dcenter.as<double>(D), st->xs);
     c->check_launch();
     CU(cudaMemcpyAsync(c->h_status, dst, sizeof(IterStatus), cudaMemcpyDeviceToHost, c->stream));
     c->sync();
