@@ -208,6 +208,7 @@ def run_ours(args):
     lib.es_ctx_set_timing(ctx.handle, 0)
     barrier(world)
     em_ms_max = max_over_ranks(em_ms, world)
+    npass = em.record_passes
     model = em.finish()
     em.close()
 
@@ -267,8 +268,11 @@ def run_ours(args):
     if rank != 0:
         return
     hbm, src = peaks()
-    ek = os.environ.get("ES_EM_KERNEL", "ws")
-    em_kernel = ("k_em_ws (warp-specialized: TMA + tcgen05 3xTF32 whitening | FP32/FP64 M-step warps)"
+    ek = os.environ.get("ES_EM_KERNEL", "mma")
+    em_kernel = (f"k_em_mma<{npass}> (tcgen05: 3xfp16 E-step whitening + block-diagonal Gram of fp16 "
+                 f"{'hi+lo ' if npass == 2 else ''}records, FP64 flush)"
+                 if ctx.precision == "mixed" and ek.startswith("m") else
+                 "k_em_ws (warp-specialized: TMA + tcgen05 3xTF32 whitening | FP32/FP64 M-step warps)"
                  if ctx.precision == "mixed" and ek.startswith("w") else
                  "k_em_tc (tcgen05 3xTF32 whitening + FP32/FP64 M-step)" if ctx.precision == "mixed" and ek == "tc" else
                  "k_em_fast<16> (SIMT FP32)" if ctx.precision == "mixed" else "k_em_team<16,2> (FP64)")
@@ -294,8 +298,8 @@ def run_ours(args):
                      "algorithmic_bytes_per_launch": bytes_iter / world, "avg_launch_ms": em_kern_avg,
                      "kernel_share_of_step": kern_ms / em_ms if em_ms else None,
                      "traffic_source": args.traffic_note,
-                     "limiter": "SIMT issue (M-step Gram ~4 significant (event, component) pairs/event, FP32 "
-                                "FFMA2) - see DESIGN.md Roofline"},
+                     "limiter": "shared-memory operand bandwidth of the block-diagonal Gram (tensor-core "
+                                "smem reads + record stores ~= 128 B/clk/SM) - see DESIGN.md section 3"},
         "score": {"events_per_s": sc_evs, "ms_per_pass": sc_ms / args.steps, "n_flagged": nflag,
                   "roofline": {"bound": "hbm", "kernel": sc_kernel, "achieved": sc_ach, "peak": hbm,
                                "unit": "GB/s", "frac": sc_ach / hbm,

@@ -148,6 +148,9 @@ int es_gmm_em_begin(es_ctx* ctx, es_dataset* ds, int32_t K, const es_fit_opts* o
 int es_gmm_em_step(es_em_state* st, int32_t n_iter, int32_t* done);
 int es_gmm_em_end(es_em_state* st, es_gmm_params* out, es_fit_report* rep, double* per_iter);
 int es_gmm_em_free(es_em_state* st);
+/* Record precision of the last fused (tcgen05) E+M pass: 1 = single fp16 record
+ * (every component had >= 2^20 events), 2 = fp16 hi + lo records, 0 = another kernel. */
+int es_gmm_em_record_passes(const es_em_state* st, int32_t* passes);
 
 /* ------------------------------------------------------------- score ---- */
 /* Per local event (any output nullable): ll = log p(x); predict = argmax

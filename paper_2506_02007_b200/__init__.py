@@ -331,6 +331,13 @@ class EM:
         self.done = bool(d.value)
         return self.done
 
+
+    @property
+    def record_passes(self) -> int:
+        """Record precision of the last fused tcgen05 E+M pass (1 or 2; 0 = another kernel)."""
+        v = C.c_int32()
+        _check(self.ctx._lib.es_gmm_em_record_passes(self.handle, C.byref(v)))
+        return v.value
     def finish(self) -> GmmModel:
         K, D = self.K, self.ds.D
         w, m, c = np.empty(K), np.empty((K, D)), np.empty((K, D, D))

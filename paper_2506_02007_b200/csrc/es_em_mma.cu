@@ -16,12 +16,12 @@
 //                 tile), FP32 over <= 8 tiles, then FP64 in shared memory.
 //
 // Records (fp16, MN-major, one 19-group row per event):
-//   group 0: s_h/2 | groups 1..16: R_h = fp16(s_k (x^ - m_k)) | 17: s_h | 18: s_l
-//   and (NPASS = 2) a second record 2 R_l = fp16(2 (r - R_h)).
-// Pass 1:  R_h^T [R_h | s_h | s_l]     (N = 144; N = 136 without s_l)
-// Pass 2:  (2 R_l)^T R_h, (2 R_l)^T (s_h/2)   (N = 128 + 8)
+//   groups 0..15: R_h = fp16(s_k (x^ - m_k)) | 16: s_h |
+//   17: s_l | 18: s_h/2, and (NPASS = 2) a second record 2 R_l = fp16(2 (r - R_h)).
+// Pass 1:  R_h^T [R_h | s_h | s_l]                      (N = 144; N = 136 without s_l)
+// Pass 2:  (2 R_l)^T R_h -> Gram columns, (2 R_l)^T (s_h/2) -> s_h columns (N = 128 + 8)
 // so that P = R_h^T R_h + 2 R_l^T R_h and sym(P) = R_h^T R_h + R_l^T R_h + R_h^T R_l
-// (the Gram to ~2^-22), and the first moment R_h s_h + R_h s_l + R_l s_h.
+// (the Gram to ~2^-21), and the first moment R_h s_h + R_h s_l + R_l s_h.
 // NPASS = 1 keeps only R_h^T [R_h | s_h] (2^-12 per-event rounding noise).
 //
 // Numerics.  tcgen05 accumulates in FP32 with truncation
@@ -55,7 +55,7 @@ constexpr uint32_t OPB = 4096;         // one 128 x 16 fp16 K-major operand
 constexpr uint32_t GRP = (TM / 8) * 128;   // one MN-major group of 8 columns: 16 K-groups x 128 B
 constexpr uint32_t RECH = 19 * GRP;        // 38912 B
 constexpr uint32_t RECL = 16 * GRP;        // 32768 B
-constexpr int MREG0 = 128, MREGS = 152;    // Gram regions at TMEM columns [128, 280) and [280, 432)
+constexpr int MREG0 = 128, MREGS = 144;    // Gram regions at TMEM columns [128, 272) and [272, 416)
 
 // kind::f16 instruction descriptor: D = F32, A = B = F16, N>>3 @17, M>>4 @24,
 // transpose (MN-major) A @15, B @16.
@@ -75,6 +75,7 @@ struct Smem {
     unsigned char bw[2][OPB];                           // W' hi / lo
     unsigned char bb[OPB];                              // b' hi, lo in K columns 0, 1
     double c[DM];
+    double ncx[DM];                                     // -c xs (exact: xs is a power of two)
     double shift[2][KMAX * DM];                         // record centre - starting centre (FP64, exact)
     double dl[2][KMAX * DM], s1x[2][KMAX * DM];         // recentring exchange
     double wred[8][KMAX + 1];                           // per-warp partial N_k | logL
@@ -104,6 +105,21 @@ __device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+__device__ __forceinline__ uint64_t sub2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ float ex2(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float lg2(float x) {
+    float r;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 __device__ __forceinline__ void commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
                  : "memory");
@@ -113,6 +129,16 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
 }
 __device__ __forceinline__ void arrive(uint64_t* b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(su32(b)), "r"(parity)
+        : "memory");
+    return done != 0;
 }
 __device__ __forceinline__ void named_sync(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
@@ -138,7 +164,6 @@ __device__ __forceinline__ void tmem_ld2(uint32_t taddr, float& a, float& b) {
     b = __uint_as_float(r1);
 }
 __device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
-__device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 // round-to-nearest, saturating fp32 pair -> fp16x2 (lo in the low half)
 __device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
     uint32_t r;
@@ -168,7 +193,10 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
     const int64_t J = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
     // ------------------------------------------------------------------ staging
-    for (int j = t; j < DM; j += NTHR) S.c[j] = j < D ? center[j] : 0.0;
+    for (int j = t; j < DM; j += NTHR) {
+        S.c[j] = j < D ? center[j] : 0.0;
+        S.ncx[j] = j < D ? -center[j] * xs : 0.0;
+    }
     for (int e = t; e < XS * DM * TM; e += NTHR) (&S.xd[0][0])[e] = 0.0;  // planes >= D stay zero
     if (t < KMAX) {
         const int k = t;
@@ -271,16 +299,15 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
         auto flush = [&](int64_t jj) {  // Gram of this WG's local tile jj -> FP64
             mbar_wait(su32(&S.mdone[w]), (uint32_t)(jj & 1));
             tc_fence_after();
-            const uint32_t rg = (uint32_t)(MREG0 + MREGS * w), xg = rg + 8;
+            const uint32_t xg = (uint32_t)(MREG0 + MREGS * w);
             float v[32], f0, f1, m1;
             tmem_ld32(tmem + lq + xg + 32 * q, v);
             tmem_ld2(tmem + lq + xg + TM + 2 * q, f0, f1);
             if (NPASS == 2) {
-                float e0, e1, c0, c1;
+                float e0, e1;
                 tmem_ld2(tmem + lq + xg + TM + KMAX + 2 * q, e0, e1);
-                tmem_ld2(tmem + lq + rg + 2 * q, c0, c1);
                 tmem_wait_ld();
-                m1 = hsel ? f1 + (e1 + c1) : f0 + (e0 + c0);
+                m1 = hsel ? f1 + e1 : f0 + e0;
             } else {
                 tmem_wait_ld();
                 m1 = hsel ? f1 : f0;
@@ -339,31 +366,27 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
 
         bool pend = false;   // the Gram of this WG's previous tile is still to be flushed
         int64_t jj = 0;      // local tile index
-        for (int64_t j = w; j < J; j += 2, ++jj) {
+        // convert tile j: x^ = (x - c) xs -> FP32 row (registers) + fp16 hi/lo operand in ae[w]
+        auto convert = [&](int64_t j, uint64_t (&x2)[DM / 2]) {
             const int s = (int)(j % XS);
-            const bool valid = tile_of(j) * TM + p < n;
-            // ---- convert: x^ = (x - c) xs -> FP32 row (registers) + fp16 hi/lo operand
             mbar_wait(su32(&S.xfull[s]), (uint32_t)((j / XS) & 1));
-            uint64_t x2[DM / 2];
-            {
-                uint32_t hw[DM / 2], lw[DM / 2];
+            uint32_t hw[DM / 2], lw[DM / 2];
 #pragma unroll
-                for (int f = 0; f < DM; f += 2) {
-                    const float v0 = (float)((S.xd[s][f * TM + p] - S.c[f]) * xs);
-                    const float v1 = (float)((S.xd[s][(f + 1) * TM + p] - S.c[f + 1]) * xs);
-                    x2[f / 2] = pack2(v0, v1);
-                    const uint32_t h = pack_h2(v0, v1);
-                    const float2 hf = __half22float2(u2h(h));
-                    hw[f / 2] = h;
-                    lw[f / 2] = pack_h2(v0 - hf.x, v1 - hf.y);
-                }
+            for (int f = 0; f < DM; f += 2) {
+                const float v0 = (float)fma(S.xd[s][f * TM + p], xs, S.ncx[f]);
+                const float v1 = (float)fma(S.xd[s][(f + 1) * TM + p], xs, S.ncx[f + 1]);
+                x2[f / 2] = pack2(v0, v1);
+                const uint32_t h = pack_h2(v0, v1);
+                const float2 hf = __half22float2(u2h(h));
+                hw[f / 2] = h;
+                lw[f / 2] = pack_h2(v0 - hf.x, v1 - hf.y);
+            }
 #pragma unroll
-                for (int g = 0; g < 2; ++g) {
-                    *reinterpret_cast<uint4*>(S.ae[w][0] + kmaj(p, 8 * g)) =
-                        make_uint4(hw[4 * g], hw[4 * g + 1], hw[4 * g + 2], hw[4 * g + 3]);
-                    *reinterpret_cast<uint4*>(S.ae[w][1] + kmaj(p, 8 * g)) =
-                        make_uint4(lw[4 * g], lw[4 * g + 1], lw[4 * g + 2], lw[4 * g + 3]);
-                }
+            for (int g = 0; g < 2; ++g) {
+                *reinterpret_cast<uint4*>(S.ae[w][0] + kmaj(p, 8 * g)) =
+                    make_uint4(hw[4 * g], hw[4 * g + 1], hw[4 * g + 2], hw[4 * g + 3]);
+                *reinterpret_cast<uint4*>(S.ae[w][1] + kmaj(p, 8 * g)) =
+                    make_uint4(lw[4 * g], lw[4 * g + 1], lw[4 * g + 2], lw[4 * g + 3]);
             }
             proxy_fence();
             named_sync(1 + w, 128);
@@ -371,6 +394,11 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
                 arrive(&S.xfree[s]);
                 arrive(&S.aeready[w]);
             }
+        };
+        uint64_t x2[DM / 2], x2n[DM / 2];
+        if (w < J) convert(w, x2);
+        for (int64_t j = w; j < J; j += 2, ++jj) {
+            const bool valid = tile_of(j) * TM + p < n;
             // ---- E-step epilogue
             mbar_wait(su32(&S.edone[w]), (uint32_t)(jj & 1));
             tc_fence_after();
@@ -395,14 +423,17 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
             tc_fence_before();
             __syncwarp();
             if (lane == 0) arrive(&S.efree);
+            // E(j) has consumed ae[w]: stage the next tile of this WG now, so that its
+            // E-step is ready long before this tile's records are
+            if (j + 2 < J) convert(j + 2, x2n);
             float ssum = 0.f;
 #pragma unroll
-            for (int k = 0; k < KMAX; ++k) ssum += exp2f((wk[k] - mx) * 1.4426950408889634f);
-            const float ll = mx + log2f(ssum) * 0.6931471805599453f;
+            for (int k = 0; k < KMAX; ++k) ssum += ex2((wk[k] - mx) * 1.4426950408889634f);
+            const float ll = mx + lg2(ssum) * 0.6931471805599453f;
             float sg[KMAX];
 #pragma unroll
             for (int k = 0; k < KMAX; ++k) {
-                sg[k] = valid ? exp2f((wk[k] - ll) * 0.7213475204444817f) : 0.f;
+                sg[k] = valid ? ex2((wk[k] - ll) * 0.7213475204444817f) : 0.f;
                 nk[k] += (double)(sg[k] * sg[k]);
             }
             if (valid) llacc += (double)ll;
@@ -428,15 +459,17 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
                         unpack2(rr, lo, hi);
                         oh[r + h] = pack_h2(lo, hi);
                         if (NPASS == 2) {
+                            // R_h rounded to nearest (a truncated R_h would bias R_l and leave
+                            // a -2^-22 diagonal bias in the dropped R_l^T R_l term)
                             const float2 hf = __half22float2(u2h(oh[r + h]));
-                            const uint64_t dd = add2(rr, pack2(-hf.x, -hf.y));
-                            unpack2(add2(dd, dd), lo, hi);
+                            const uint64_t dd = sub2(rr, pack2(hf.x, hf.y));
+                            unpack2(add2(dd, dd), lo, hi);  // 2 R_l (exact doubling)
                             ol[r + h] = pack_h2(lo, hi);
                         }
                     }
                 }
-                *reinterpret_cast<uint4*>(rh + (1 + 2 * k) * GRP) = make_uint4(oh[0], oh[1], oh[2], oh[3]);
-                *reinterpret_cast<uint4*>(rh + (2 + 2 * k) * GRP) = make_uint4(oh[4], oh[5], oh[6], oh[7]);
+                *reinterpret_cast<uint4*>(rh + (2 * k) * GRP) = make_uint4(oh[0], oh[1], oh[2], oh[3]);
+                *reinterpret_cast<uint4*>(rh + (2 * k + 1) * GRP) = make_uint4(oh[4], oh[5], oh[6], oh[7]);
                 if (NPASS == 2) {
                     *reinterpret_cast<uint4*>(rl + (2 * k) * GRP) = make_uint4(ol[0], ol[1], ol[2], ol[3]);
                     *reinterpret_cast<uint4*>(rl + (2 * k + 1) * GRP) = make_uint4(ol[4], ol[5], ol[6], ol[7]);
@@ -446,18 +479,17 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
                 uint32_t sh[4];
 #pragma unroll
                 for (int r = 0; r < 4; ++r) sh[r] = pack_h2(sg[2 * r], sg[2 * r + 1]);
-                *reinterpret_cast<uint4*>(rh + 17 * GRP) = make_uint4(sh[0], sh[1], sh[2], sh[3]);
+                *reinterpret_cast<uint4*>(rh + 16 * GRP) = make_uint4(sh[0], sh[1], sh[2], sh[3]);
                 if (NPASS == 2) {
                     uint32_t sl[4], s5[4];
-                    const __half2 half2_05 = __float2half2_rn(0.5f);
 #pragma unroll
                     for (int r = 0; r < 4; ++r) {
                         const float2 hf = __half22float2(u2h(sh[r]));
                         sl[r] = pack_h2(sg[2 * r] - hf.x, sg[2 * r + 1] - hf.y);
-                        s5[r] = h2u(__hmul2(u2h(sh[r]), half2_05));
+                        s5[r] = pack_h2(0.5f * hf.x, 0.5f * hf.y);  // s_h / 2, exact
                     }
-                    *reinterpret_cast<uint4*>(rh + 18 * GRP) = make_uint4(sl[0], sl[1], sl[2], sl[3]);
-                    *reinterpret_cast<uint4*>(rh) = make_uint4(s5[0], s5[1], s5[2], s5[3]);
+                    *reinterpret_cast<uint4*>(rh + 17 * GRP) = make_uint4(sl[0], sl[1], sl[2], sl[3]);
+                    *reinterpret_cast<uint4*>(rh + 18 * GRP) = make_uint4(s5[0], s5[1], s5[2], s5[3]);
                 }
             }
             proxy_fence();
@@ -470,6 +502,8 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
                 pend = false;
                 recentre(false);
             }
+#pragma unroll
+            for (int r = 0; r < DM / 2; ++r) x2[r] = x2n[r];
         }
         if (pend) flush(jj - 1);
         recentre(true);
@@ -536,38 +570,54 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
             constexpr uint32_t idesc1 = idesc_f16(128, NPASS == 2 ? 144 : 136, 1);
             constexpr uint32_t idesc2a = idesc_f16(128, 128, 1);
             constexpr uint32_t idesc2b = idesc_f16(128, 8, 1);
+            // pass 1: D1 = R_h^T [R_h | s_h | s_l]; pass 2: P = D1 + (2 R_l)^T R_h on the Gram
+            // columns, + (2 R_l)^T (s_h / 2) = R_l^T s_h on the s_h columns.
             auto gram = [&](int64_t m) {
                 const int mw = (int)(m & 1);
-                mbar_wait_sleep(su32(&S.mready[mw]), (uint32_t)((m >> 1) & 1));
                 tc_fence_after();
-                const uint32_t rg = tmem + (uint32_t)(MREG0 + MREGS * mw), xg = rg + 8;
+                const uint32_t xg = tmem + (uint32_t)(MREG0 + MREGS * mw);
                 const uint32_t h0 = su32(S.rech[mw]), l0 = su32(S.recl[mw]);
 #pragma unroll
                 for (int ks = 0; ks < TM / 16; ++ks) {
-                    const uint64_t dh = sdesc(h0 + GRP + ks * 256, 128, GRP);  // groups 1.. (R_h, s_h, s_l)
+                    const uint64_t dh = sdesc(h0 + ks * 256, 128, GRP);
                     mma_f16(xg, dh, dh, idesc1, ks > 0 ? 1u : 0u);
-                    if (NPASS == 2) {
+                }
+                if (NPASS == 2) {
+#pragma unroll
+                    for (int ks = 0; ks < TM / 16; ++ks) {
+                        const uint64_t dh = sdesc(h0 + ks * 256, 128, GRP);
                         const uint64_t dl = sdesc(l0 + ks * 256, 128, GRP);
                         mma_f16(xg, dl, dh, idesc2a, 1u);
-                        mma_f16(rg, dl, sdesc(h0 + ks * 256, 128, GRP), idesc2b, ks > 0 ? 1u : 0u);
+                        mma_f16(xg + TM, dl, sdesc(h0 + 18 * GRP + ks * 256, 128, GRP), idesc2b, 1u);
                     }
                 }
                 commit(&S.mdone[mw]);
             };
-            for (int64_t j = 0; j < J; ++j) {
-                const int w = (int)(j & 1);
-                mbar_wait_sleep(su32(&S.aeready[w]), (uint32_t)((j >> 1) & 1));
-                if (j >= 1) mbar_wait_sleep(su32(&S.efree), (uint32_t)((j - 1) & 1));
-                tc_fence_after();
-                const uint64_t dah = sdesc(su32(S.ae[w][0]), 128, 256), dal = sdesc(su32(S.ae[w][1]), 128, 256);
-                mma_f16(tmem, dah, dbh, kIdescE, 0u);
-                mma_f16(tmem, dah, dbl, kIdescE, 1u);
-                mma_f16(tmem, dal, dbh, kIdescE, 1u);
-                mma_f16(tmem, done, dbb, kIdescE, 1u);
-                commit(&S.edone[w]);
-                if (j >= 1) gram(j - 1);
+            // issue whichever of the next E-step / next Gram is ready, E first: the
+            // warpgroups' critical path runs through E, the Gram only has to keep up
+            int64_t je = 0, jm = 0;
+            while (jm < J) {
+                bool did = false;
+                if (je < J && mbar_test(&S.aeready[je & 1], (uint32_t)((je >> 1) & 1)) &&
+                    (je == 0 || mbar_test(&S.efree, (uint32_t)((je - 1) & 1)))) {
+                    const int w = (int)(je & 1);
+                    tc_fence_after();
+                    const uint64_t dah = sdesc(su32(S.ae[w][0]), 128, 256), dal = sdesc(su32(S.ae[w][1]), 128, 256);
+                    mma_f16(tmem, dah, dbh, kIdescE, 0u);
+                    mma_f16(tmem, dah, dbl, kIdescE, 1u);
+                    mma_f16(tmem, dal, dbh, kIdescE, 1u);
+                    mma_f16(tmem, done, dbb, kIdescE, 1u);
+                    commit(&S.edone[w]);
+                    ++je;
+                    did = true;
+                }
+                if (jm < je && mbar_test(&S.mready[jm & 1], (uint32_t)((jm >> 1) & 1))) {
+                    gram(jm);
+                    ++jm;
+                    did = true;
+                }
+                if (!did) __nanosleep(32);
             }
-            if (J >= 1) gram(J - 1);
         }
     }
     tc_fence_before();
@@ -585,11 +635,12 @@ bool em_mma_enabled() {
     return v == 1;
 }
 
+// ES_EM_MMA_PASSES=1|2 forces the record precision; otherwise (0) the caller decides.
 int em_mma_passes() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("ES_EM_MMA_PASSES");
-        v = (e && e[0] == '1') ? 1 : 2;
+        v = (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
     }
     return v;
 }
@@ -607,11 +658,12 @@ static void launch_npass(const CUtensorMap* xmap, int64_t n, int D, int K, const
 }
 
 void launch_em_mma(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model, const double* center,
-                   double xs, double* partial, int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls) {
+                   double xs, int npass, double* partial, int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls) {
     const int64_t ntiles = (n + TM - 1) / TM;
     const int grid = (int)std::min<int64_t>(num_sms, std::max<int64_t>(ntiles, 1));
     *nblk = grid;
-    if (em_mma_passes() == 1)
+    if (em_mma_passes() != 0) npass = em_mma_passes();
+    if (npass == 1)
         launch_npass<1>(xmap, n, D, K, model, center, xs, partial, grid, s);
     else
         launch_npass<2>(xmap, n, D, K, model, center, xs, partial, grid, s);

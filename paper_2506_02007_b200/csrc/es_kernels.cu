@@ -1109,6 +1109,8 @@ __global__ void k_finalize(const double* __restrict__ stats, int G, int D, int K
     }
     __syncthreads();
     const double Nk = sS[0];
+    if (threadIdx.x == 0 && Nk >= 0.0)
+        atomicMax((unsigned long long*)&st->min_nk_inv, ~(unsigned long long)__double_as_longlong(Nk));
     if (!(Nk >= 1.0)) {  // collapse: N * pi_k < 1; host reseeds
         if (threadIdx.x == 0) {
             if (k < 64) atomicOr((unsigned long long*)&st->collapse_lo, 1ull << k);

@@ -96,9 +96,12 @@ void launch_em_ws(const CUtensorMap* xmap, int64_t n, int D, int K, const double
 // Fused pass with E-step and M-step Gram on tcgen05 (es_em_mma.cu), the default
 // for D <= 16, K <= 8 (ES_EM_KERNEL=mma|ws|tc|simt).  Writes finalize mode-3 statistics.
 bool em_mma_enabled();
-int em_mma_passes();  // 2 (hi + lo records, default) or 1 (ES_EM_MMA_PASSES=1)
+// Record precision: npass 2 (fp16 hi + lo records) or 1 (single fp16 record, used when
+// every component has >= kOnePassMinNk events); ES_EM_MMA_PASSES=1|2 overrides.
+constexpr double kOnePassMinNk = 1048576.0;
+int em_mma_passes();
 void launch_em_mma(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model, const double* center,
-                   double xs, double* partial, int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
+                   double xs, int npass, double* partial, int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
 // Builds that tensor map (driver entry point resolved through the runtime).
 bool make_event_tmap(CUtensorMap* map, const double* X, int64_t n, int64_t ld, int D);
 // tcgen05 scoring pass (es_score_tc.cu); ES_SCORE_KERNEL=simt selects k_score_fast.

@@ -52,6 +52,7 @@ struct IterStatus {
     uint64_t collapse_hi;    // components 64..127
     int32_t not_pd;          // a new covariance failed Cholesky
     int32_t pad;
+    uint64_t min_nk_inv;     // ~bits(min_k N_k) (max-reduced; 0 = none): picks the record precision
 };
 
 }  // namespace es

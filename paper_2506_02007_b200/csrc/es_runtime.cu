@@ -272,6 +272,8 @@ struct es_em_state {
     std::vector<double> S;  // data covariance (D x D)
     std::vector<double> mean;  // data mean: FP64 centre of the mixed-precision path
     double xs = 1.0;           // power of two bringing max|x - mean| into (8, 16] (k_em_mma operand scale)
+    double min_nk = 0.0;       // min_k N_k of the current model (global), selects k_em_mma's record precision
+    int last_npass = 0;        // record precision of the last k_em_mma pass (0: other kernel)
     DevBuf dcenter;
     SplitMix64 rng{0};
     std::vector<double> per_iter;
@@ -611,6 +613,7 @@ void em_init_model(es_em_state* st, const es_gmm_params* init, const DataStats& 
     }
     double* m = c->model.as<double>(mstride(K, D));
     upload_model(c, m, K, D, pi.data(), mu.data(), cov.data());
+    st->min_nk = (double)ds->n_global * *std::min_element(pi.begin(), pi.end());
 }
 
 void em_begin(es_em_state* st, const es_gmm_params* init) {
@@ -671,8 +674,10 @@ bool em_iterate(es_em_state* st) {
         bool wh = true, wh_mma = false;
         if (c->precision == 0 && em_fast_supported(D, K)) {
             if (em_mma_enabled() && ds->has_xmap) {
-                launch_em_mma(&ds->xmap, ds->n_local, D, K, dmodel, st->dcenter.as<double>(D), st->xs, part,
+                const int np = st->min_nk >= kOnePassMinNk ? 1 : 2;
+                launch_em_mma(&ds->xmap, ds->n_local, D, K, dmodel, st->dcenter.as<double>(D), st->xs, np, part,
                               c->num_sms, &nblk, c->stream, c->ls);
+                st->last_npass = em_mma_passes() ? em_mma_passes() : np;
                 wh_mma = true;
             } else if (em_ws_enabled() && ds->has_xmap)
                 launch_em_ws(&ds->xmap, ds->n_local, D, K, dmodel, st->dcenter.as<double>(D), part, c->num_sms,
@@ -712,6 +717,7 @@ bool em_iterate(es_em_state* st) {
     c->sync();
     const IterStatus s = *c->h_status;
     const double cur = s.logL;
+    if (s.min_nk_inv) st->min_nk = __builtin_bit_cast(double, ~(unsigned long long)s.min_nk_inv);
     st->per_iter.push_back(cur);
     st->last = cur;
     const int t = st->t++;
@@ -737,6 +743,7 @@ bool em_iterate(es_em_state* st) {
             const bool col = k < 64 ? ((s.collapse_lo >> k) & 1) : ((s.collapse_hi >> (k - 64)) & 1);
             if (!col) continue;
             if (++st->collapses > 2) fail(ES_ERR_NUMERIC, "RepeatedCollapse", "component collapsed more than twice");
+            st->min_nk = 0.0;  // a reseeded component: two-pass records next iteration
             const int64_t r = (int64_t)st->rng.below((uint64_t)ds->n_global);
             std::vector<double> row;
             fetch_rows(c, ds, {r}, row);
@@ -1049,6 +1056,13 @@ int es_gmm_em_begin(es_ctx* c, es_dataset* ds, int32_t K, const es_fit_opts* opt
         st->opts = *opts;
         em_begin(st.get(), init);
         *out = st.release();
+    });
+}
+
+int es_gmm_em_record_passes(const es_em_state* st, int32_t* passes) {
+    return guard([&] {
+        if (!st || !passes) fail(ES_ERR_DATA, "InvalidArgument", "null state or output");
+        *passes = st->last_npass;
     });
 }
 
