@@ -50,12 +50,13 @@ using namespace tc;
 
 constexpr int DM = 16, KMAX = 8, TM = 128;
 constexpr int NTHR = 320;              // WG0, WG1 (alternate tiles), warp 8 TMA, warp 9 MMA
-constexpr int XS = 2;                  // FP64 tile stages (TMA)
 constexpr uint32_t OPB = 4096;         // one 128 x 16 fp16 K-major operand
 constexpr uint32_t GRP = (TM / 8) * 128;   // one MN-major group of 8 columns: 16 K-groups x 128 B
 constexpr uint32_t RECH = 19 * GRP;        // 38912 B
 constexpr uint32_t RECL = 16 * GRP;        // 32768 B
 constexpr int MREG0 = 128, MREGS = 144;    // Gram regions at TMEM columns [128, 272) and [272, 416)
+constexpr int TA0 = 416;                   // x^ hi/lo E-step A operands: WG w at [416 + 16 w, +16)
+constexpr int TONE = 448;                  // ones in K columns 0, 1 (bias dispatch A operand)
 
 // kind::f16 instruction descriptor: D = F32, A = B = F16, N>>3 @17, M>>4 @24,
 // transpose (MN-major) A @15, B @16.
@@ -67,15 +68,13 @@ constexpr uint32_t kIdescE = idesc_f16(128, 128, 0);
 
 template <int NPASS>
 struct Smem {
-    double xd[XS][DM * TM];                             // 32 KB  FP64 tiles (planar, TMA destination)
+    static constexpr int XS = NPASS == 2 ? 3 : 4;       // FP64 tile stages (TMA)
+    double xd[XS][DM * TM];                             // 48 / 64 KB  FP64 tiles (planar, TMA destination)
     unsigned char rech[2][RECH];                        // 76 KB  hi records (per warpgroup)
     unsigned char recl[2][NPASS == 2 ? RECL : 16];      // 64 KB  2 x lo records
-    unsigned char ae[2][2][OPB];                        // 16 KB  x^ hi / lo (per warpgroup)
-    unsigned char aone[OPB];                            // ones in K columns 0, 1
     unsigned char bw[2][OPB];                           // W' hi / lo
     unsigned char bb[OPB];                              // b' hi, lo in K columns 0, 1
     double c[DM];
-    double ncx[DM];                                     // -c xs (exact: xs is a power of two)
     double shift[2][KMAX * DM];                         // record centre - starting centre (FP64, exact)
     double dl[2][KMAX * DM], s1x[2][KMAX * DM];         // recentring exchange
     double wred[8][KMAX + 1];                           // per-warp partial N_k | logL
@@ -86,6 +85,11 @@ struct Smem {
     float tk[KMAX];
     uint64_t xfull[XS], xfree[XS], aeready[2], edone[2], mready[2], mdone[2], efree;
     uint32_t tmem;
+};
+
+// -c xs per feature (kernel parameter: constant-bank operands, no shared-memory loads)
+struct NegCx {
+    double v[DM];
 };
 
 // byte offset of (row, k) in a K-major 128 x 16 fp16 operand (SWIZZLE_NONE core matrices)
@@ -104,6 +108,17 @@ __device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_f16_ta(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
 }
 __device__ __forceinline__ uint64_t sub2(uint64_t a, uint64_t b) {
     uint64_t r;
@@ -182,8 +197,10 @@ template <int NPASS>
 __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUtensorMap xmap, int64_t n, int D,
                                                      int K, const double* __restrict__ model,
                                                      const double* __restrict__ center, double xs,
+                                                     const __grid_constant__ NegCx ncx,
                                                      double* __restrict__ partial) {
     using Sm = Smem<NPASS>;
+    constexpr int XS = Sm::XS;
     extern __shared__ __align__(128) unsigned char smraw[];
     // keep the shared-window provenance of the pointer (generic LD/ST otherwise)
     Sm& S = *reinterpret_cast<Sm*>(smraw + ((128u - (su32(smraw) & 127u)) & 127u));
@@ -193,10 +210,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
     const int64_t J = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
     // ------------------------------------------------------------------ staging
-    for (int j = t; j < DM; j += NTHR) {
-        S.c[j] = j < D ? center[j] : 0.0;
-        S.ncx[j] = j < D ? -center[j] * xs : 0.0;
-    }
+    for (int j = t; j < DM; j += NTHR) S.c[j] = j < D ? center[j] : 0.0;
     for (int e = t; e < XS * DM * TM; e += NTHR) (&S.xd[0][0])[e] = 0.0;  // planes >= D stay zero
     if (t < KMAX) {
         const int k = t;
@@ -246,7 +260,6 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
         const __half bh = __double2half(b);
         const __half bl = __double2half(b - (double)__half2float(bh));
         *reinterpret_cast<__half*>(S.bb + kmaj(row, f)) = f == 0 ? bh : (f == 1 ? bl : __half(0.f));
-        *reinterpret_cast<__half*>(S.aone + kmaj(row, f)) = __half(f < 2 ? 1.f : 0.f);
     }
     if (warp == 9) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&S.tmem)));
@@ -272,6 +285,14 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
     tc_fence_after();
     const uint32_t tmem = S.tmem;
     auto tile_of = [&](int64_t j) { return (int64_t)blockIdx.x + j * gridDim.x; };
+    if (warp < 4) {  // ones in K columns 0, 1 of every row: the bias dispatch's A operand
+        const uint32_t one[8] = {0x3C003C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+        tmem_st8(tmem + ((uint32_t)(32 * warp) << 16) + TONE, one);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
 
     if (warp < 8) {
         // ====================================================== epilogue warpgroups
@@ -366,29 +387,26 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
 
         bool pend = false;   // the Gram of this WG's previous tile is still to be flushed
         int64_t jj = 0;      // local tile index
-        // convert tile j: x^ = (x - c) xs -> FP32 row (registers) + fp16 hi/lo operand in ae[w]
+        // convert tile j: x^ = (x - c) xs -> FP32 row (registers) + fp16 hi/lo E-step A operand
+        // in this WG's TMEM columns (lane = event, tcgen05.st)
         auto convert = [&](int64_t j, uint64_t (&x2)[DM / 2]) {
             const int s = (int)(j % XS);
             mbar_wait(su32(&S.xfull[s]), (uint32_t)((j / XS) & 1));
             uint32_t hw[DM / 2], lw[DM / 2];
 #pragma unroll
             for (int f = 0; f < DM; f += 2) {
-                const float v0 = (float)fma(S.xd[s][f * TM + p], xs, S.ncx[f]);
-                const float v1 = (float)fma(S.xd[s][(f + 1) * TM + p], xs, S.ncx[f + 1]);
+                const float v0 = (float)fma(S.xd[s][f * TM + p], xs, ncx.v[f]);
+                const float v1 = (float)fma(S.xd[s][(f + 1) * TM + p], xs, ncx.v[f + 1]);
                 x2[f / 2] = pack2(v0, v1);
                 const uint32_t h = pack_h2(v0, v1);
                 const float2 hf = __half22float2(u2h(h));
                 hw[f / 2] = h;
                 lw[f / 2] = pack_h2(v0 - hf.x, v1 - hf.y);
             }
-#pragma unroll
-            for (int g = 0; g < 2; ++g) {
-                *reinterpret_cast<uint4*>(S.ae[w][0] + kmaj(p, 8 * g)) =
-                    make_uint4(hw[4 * g], hw[4 * g + 1], hw[4 * g + 2], hw[4 * g + 3]);
-                *reinterpret_cast<uint4*>(S.ae[w][1] + kmaj(p, 8 * g)) =
-                    make_uint4(lw[4 * g], lw[4 * g + 1], lw[4 * g + 2], lw[4 * g + 3]);
-            }
-            proxy_fence();
+            tmem_st8(tmem + lq + TA0 + 16 * w, hw);
+            tmem_st8(tmem + lq + TA0 + 16 * w + 8, lw);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
             named_sync(1 + w, 128);
             if (p == 0) {
                 arrive(&S.xfree[s]);
@@ -423,7 +441,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
             tc_fence_before();
             __syncwarp();
             if (lane == 0) arrive(&S.efree);
-            // E(j) has consumed ae[w]: stage the next tile of this WG now, so that its
+            // E(j) has consumed this WG's A operand: stage the next tile now, so that its
             // E-step is ready long before this tile's records are
             if (j + 2 < J) convert(j + 2, x2n);
             float ssum = 0.f;
@@ -566,7 +584,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
         // ========================================================== MMA issuer
         if (lane == 0) {
             const uint64_t dbh = sdesc(su32(S.bw[0]), 128, 256), dbl = sdesc(su32(S.bw[1]), 128, 256);
-            const uint64_t dbb = sdesc(su32(S.bb), 128, 256), done = sdesc(su32(S.aone), 128, 256);
+            const uint64_t dbb = sdesc(su32(S.bb), 128, 256);
             constexpr uint32_t idesc1 = idesc_f16(128, NPASS == 2 ? 144 : 136, 1);
             constexpr uint32_t idesc2a = idesc_f16(128, 128, 1);
             constexpr uint32_t idesc2b = idesc_f16(128, 8, 1);
@@ -602,11 +620,11 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
                     (je == 0 || mbar_test(&S.efree, (uint32_t)((je - 1) & 1)))) {
                     const int w = (int)(je & 1);
                     tc_fence_after();
-                    const uint64_t dah = sdesc(su32(S.ae[w][0]), 128, 256), dal = sdesc(su32(S.ae[w][1]), 128, 256);
-                    mma_f16(tmem, dah, dbh, kIdescE, 0u);
-                    mma_f16(tmem, dah, dbl, kIdescE, 1u);
-                    mma_f16(tmem, dal, dbh, kIdescE, 1u);
-                    mma_f16(tmem, done, dbb, kIdescE, 1u);
+                    const uint32_t tah = tmem + TA0 + 16 * w, tal = tah + 8;
+                    mma_f16_ta(tmem, tah, dbh, kIdescE, 0u);
+                    mma_f16_ta(tmem, tah, dbl, kIdescE, 1u);
+                    mma_f16_ta(tmem, tal, dbh, kIdescE, 1u);
+                    mma_f16_ta(tmem, tmem + TONE, dbb, kIdescE, 1u);
                     commit(&S.edone[w]);
                     ++je;
                     did = true;
@@ -647,26 +665,30 @@ int em_mma_passes() {
 
 template <int NPASS>
 static void launch_npass(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model,
-                         const double* center, double xs, double* partial, int grid, cudaStream_t s) {
+                         const double* center, double xs, const NegCx& ncx, double* partial, int grid,
+                         cudaStream_t s) {
     const size_t smem = sizeof(Smem<NPASS>) + 128;
     static bool a = false;
     if (!a) {
         cudaFuncSetAttribute(k_em_mma<NPASS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         a = true;
     }
-    k_em_mma<NPASS><<<grid, NTHR, smem, s>>>(*xmap, n, D, K, model, center, xs, partial);
+    k_em_mma<NPASS><<<grid, NTHR, smem, s>>>(*xmap, n, D, K, model, center, xs, ncx, partial);
 }
 
 void launch_em_mma(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model, const double* center,
-                   double xs, int npass, double* partial, int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls) {
+                   const double* center_host, double xs, int npass, double* partial, int num_sms, int* nblk,
+                   cudaStream_t s, LaunchStats& ls) {
+    NegCx ncx{};
+    for (int j = 0; j < D && j < DM; ++j) ncx.v[j] = -center_host[j] * xs;
     const int64_t ntiles = (n + TM - 1) / TM;
     const int grid = (int)std::min<int64_t>(num_sms, std::max<int64_t>(ntiles, 1));
     *nblk = grid;
     if (em_mma_passes() != 0) npass = em_mma_passes();
     if (npass == 1)
-        launch_npass<1>(xmap, n, D, K, model, center, xs, partial, grid, s);
+        launch_npass<1>(xmap, n, D, K, model, center, xs, ncx, partial, grid, s);
     else
-        launch_npass<2>(xmap, n, D, K, model, center, xs, partial, grid, s);
+        launch_npass<2>(xmap, n, D, K, model, center, xs, ncx, partial, grid, s);
     ++ls.launches;
 }
 

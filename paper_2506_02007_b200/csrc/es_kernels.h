@@ -101,7 +101,8 @@ bool em_mma_enabled();
 constexpr double kOnePassMinNk = 1048576.0;
 int em_mma_passes();
 void launch_em_mma(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model, const double* center,
-                   double xs, int npass, double* partial, int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
+                   const double* center_host, double xs, int npass, double* partial, int num_sms, int* nblk,
+                   cudaStream_t s, LaunchStats& ls);
 // Builds that tensor map (driver entry point resolved through the runtime).
 bool make_event_tmap(CUtensorMap* map, const double* X, int64_t n, int64_t ld, int D);
 // tcgen05 scoring pass (es_score_tc.cu); ES_SCORE_KERNEL=simt selects k_score_fast.

@@ -675,8 +675,8 @@ bool em_iterate(es_em_state* st) {
         if (c->precision == 0 && em_fast_supported(D, K)) {
             if (em_mma_enabled() && ds->has_xmap) {
                 const int np = st->min_nk >= kOnePassMinNk ? 1 : 2;
-                launch_em_mma(&ds->xmap, ds->n_local, D, K, dmodel, st->dcenter.as<double>(D), st->xs, np, part,
-                              c->num_sms, &nblk, c->stream, c->ls);
+                launch_em_mma(&ds->xmap, ds->n_local, D, K, dmodel, st->dcenter.as<double>(D), st->mean.data(),
+                              st->xs, np, part, c->num_sms, &nblk, c->stream, c->ls);
                 st->last_npass = em_mma_passes() ? em_mma_passes() : np;
                 wh_mma = true;
             } else if (em_ws_enabled() && ds->has_xmap)

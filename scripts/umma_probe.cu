@@ -227,6 +227,65 @@ __global__ void k_accum(const __half* A, const __half* B, int R, float* out) {
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tm));
 }
 
+
+// A from TMEM: thread m writes row m of A (16 fp16 = 8 x 32-bit columns) with tcgen05.st, B K-major in smem
+__global__ void k_atmem(const __half* A, const __half* B, float* out) {
+    extern __shared__ __align__(1024) unsigned char sm[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int t = threadIdx.x, warp = t >> 5;
+    for (int e = t; e < 128 * 16; e += blockDim.x) {
+        const int r = e / 16, k = e % 16;
+        const uint32_t off = (r / 8) * 256 + (k / 8) * 128 + (r % 8) * 16 + (k % 8) * 2;
+        *reinterpret_cast<__half*>(sm + off) = B[e];
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(&tbase)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (t == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tm = tbase;
+    {   // row t of A -> TMEM lane t, columns 160..167
+        uint32_t r[8];
+        for (int c = 0; c < 8; ++c) {
+            __half2 h = __halves2half2(A[t * 16 + 2 * c], A[t * 16 + 2 * c + 1]);
+            r[c] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                         tm + ((uint32_t)(32 * warp) << 16) + 160),
+                     "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                     : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (t == 0) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tm), "r"(tm + 160),
+            "l"(desc(su32(sm), 128, 256)), "r"(idesc_f16(128, 128, 0, 0)), "r"(0));
+        commit(&bar);
+    }
+    mbar_wait(&bar, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    for (int c0 = 0; c0 < 128; c0 += 32) {
+        float v[32];
+        ld32(tm + ((uint32_t)(32 * warp) << 16) + c0, v);
+        for (int j = 0; j < 32; ++j) out[t * 128 + c0 + j] = v[j];
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tm));
+}
+
 #define CK(x)                                                                                  \
     do {                                                                                       \
         cudaError_t e_ = (x);                                                                  \
@@ -282,6 +341,24 @@ int main() {
                maxerr <= 1e-5 * maxref ? "OK" : "MISMATCH");
     }
 
+
+    {   // A from TMEM check
+        float* d3;
+        CK(cudaMalloc(&d3, 128 * 128 * 4));
+        CK(cudaFuncSetAttribute(k_atmem, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192));
+        k_atmem<<<1, 128, 8192>>>(dA, dB, d3);
+        CK(cudaDeviceSynchronize());
+        std::vector<float> o(128 * 128);
+        CK(cudaMemcpy(o.data(), d3, o.size() * 4, cudaMemcpyDeviceToHost));
+        double maxerr = 0;
+        for (int m = 0; m < 128; ++m)
+            for (int n = 0; n < 128; ++n) {
+                double ref = 0;
+                for (int k = 0; k < 16; ++k) ref += Ad[m * 16 + k] * Bd[n * 16 + k];
+                maxerr = fmax(maxerr, fabs(ref - o[m * 128 + n]));
+            }
+        printf("A-in-TMEM check: max|err| %.3e -> %s\n", maxerr, maxerr < 1e-3 ? "OK" : "MISMATCH");
+    }
     for (int mode = 0; mode < 3; ++mode) {   // accumulation rounding: all +, all -, mixed signs
         const int R = 12;
         std::vector<__half> a(R * 2048), b(R * 2048);

@@ -235,3 +235,39 @@ def test_diag_fit_parity(es, oracle, D, K, n, iters):
                        rtol=LL_TOL)
     best, bic = es.select_k_bic(ds, [K], init="random", max_iter=3, seed=5, covariance_type="diag")
     assert best == K and np.isfinite(bic[0])
+
+
+# ------------------------------------------- full-size fused-kernel parity
+def test_full_size_one_pass_records_vs_fp64(es):
+    """At N = 2^25 every component has >= 2^20 events, so the fused tcgen05 pass
+    uses its single-fp16-record precision.  The strict FP64
+    kernel (itself pinned to the oracle above) is the reference at this size: the
+    oracle would need minutes per iteration here."""
+    n, D, K, iters = 1 << 25, 16, 8, 6
+    fits = {}
+    for prec in ("mixed", "fp64"):
+        ctx = es.Context(0, precision=prec)
+        ds = es.Dataset.generate(42, n, D, K, ctx=ctx)
+        em = es.EM(ds, K, init="random", tol=0.0, max_iter=iters, seed=7)
+        em.step(iters)
+        passes = em.record_passes
+        fits[prec] = (em.finish(), passes)
+        em.close()
+        ds.close()
+    (m, passes), (r, _) = fits["mixed"], fits["fp64"]
+    assert passes == 1
+    assert_params(m, r.weights, r.means, r.covariances)
+    per_m, per_r = m.fit_report.per_iteration_log_likelihoods, r.fit_report.per_iteration_log_likelihoods
+    assert np.all(np.abs(per_m - per_r) <= LL_TOL * np.abs(per_r))
+
+
+def test_two_pass_records_small_components(es, oracle):
+    """Below 2^20 events per component the fused pass switches to hi + lo records."""
+    ds, X = syn(es, oracle, 1 << 18, 16, 8)
+    em = es.EM(ds, 8, init="random", tol=0.0, max_iter=8, seed=7)
+    em.step(8)
+    assert em.record_passes == 2
+    m = em.finish()
+    em.close()
+    pi, mu, cov, rep = oracle.fit_em(X, 8, init="random", tol=0.0, max_iter=8, seed=7)
+    assert_params(m, pi, mu, cov)
