@@ -33,9 +33,9 @@ struct SmemS {
     unsigned char Ah[2][kOpBytes], Al[2][kOpBytes];   // [sub-tile]
     double xd[3][DM * TT];                            // TMA tiles (planar), triple-buffered
     double lnv[KMAX * TT];                            // FP64 log densities of refined (k, event)
-    uint16_t cev[KMAX * TT];                          // compacted candidate list: event
-    uint8_t ccomp[KMAX * TT];                         //                            component
-    int wcnt[8], woff[8], ncand;
+    uint16_t cev[KMAX * TT + KMAX];                   // compacted candidate list: event
+    uint8_t ccomp[KMAX * TT + KMAX];                  //                            component
+    int wcnt[KMAX * 8], woff[KMAX * 8], ncand;
     alignas(16) double W64[KMAX * W64S];
     double mu64[KMAX * (DM + 2)];
     double ln64[KMAX], lp64[KMAX];
@@ -221,62 +221,76 @@ __global__ void __launch_bounds__(TT, 1) k_score_tc(const __grid_constant__ CUte
                     (ln[k] == bl && fabsf(bl - ldf) <= 1e-3f * (1.f + fabsf(ldf)));
             if (valid && k < K && c) cand |= 1u << k;
         }
-        // deterministic compaction of (event, component) candidates
-        int mine = __popc(cand);
-        int incl = mine;
+        // deterministic component-major compaction of (event, component) candidates: the
+        // warps of the refinement then mostly share one component, so its FP64 W rows and
+        // mean are shared-memory broadcasts instead of up to 8 distinct rows per load
+        unsigned kb[KMAX];
 #pragma unroll
-        for (int o2 = 1; o2 < 32; o2 <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, incl, o2);
-            if (lane >= o2) incl += v;
+        for (int k = 0; k < KMAX; ++k) {
+            kb[k] = __ballot_sync(0xffffffffu, (cand >> k) & 1u);
+            if (lane == 0) S.wcnt[k * 8 + warp] = __popc(kb[k]);
         }
-        if (lane == 31) S.wcnt[warp] = incl;
         __syncthreads();  // TMEM drained; A operand free; wcnt visible
         if (t == 0) {
             int a2 = 0;
-            for (int wv = 0; wv < 8; ++wv) {
-                S.woff[wv] = a2;
-                a2 += S.wcnt[wv];
+            for (int k = 0; k < KMAX; ++k) {  // (component, warp) order; each component's
+                for (int wv = 0; wv < 8; ++wv) {  // segment padded to an even length
+                    S.woff[k * 8 + wv] = a2;
+                    a2 += S.wcnt[k * 8 + wv];
+                }
+                if (a2 & 1) {
+                    S.cev[a2] = 0xFFFFu;
+                    S.ccomp[a2] = (uint8_t)k;
+                    ++a2;
+                }
             }
             S.ncand = a2;
             prefetch(j + 2);
         }
         __syncthreads();
-        {
-            int pos = S.woff[warp] + incl - mine;
-            unsigned rem = cand;
-            while (rem) {
-                const int k = __ffs(rem) - 1;
-                rem &= rem - 1;
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) {
+            if ((cand >> k) & 1u) {
+                const int pos = S.woff[k * 8 + warp] + __popc(kb[k] & lt_mask);
                 S.cev[pos] = (uint16_t)t;
                 S.ccomp[pos] = (uint8_t)k;
-                ++pos;
             }
         }
         __syncthreads();
         if (j + 1 < my_tiles) aprep_and_mma(j + 1);  // MMA(j+1) overlaps the FP64 refinement of tile j
-        // FP64 refinement, one (event, component) pair per thread at a time
+        // FP64 refinement, two events of one component per thread (each W row load serves both)
         const int nc = S.ncand;
-        for (int pidx = t; pidx < nc; pidx += TT) {
-            const int ev = S.cev[pidx], k = S.ccomp[pidx];
+        for (int pidx = 2 * t; pidx < nc; pidx += 2 * TT) {
+            const int k = S.ccomp[pidx];
+            const int e0 = S.cev[pidx], e1r = S.cev[pidx + 1];
+            const int e1 = e1r == 0xFFFF ? e0 : e1r;
             const double* Wk = S.W64 + k * W64S;
             const double* mk = S.mu64 + k * (DM + 2);
-            const int h = ev >> 7, rw = ev & 127;
-            double dd[DM];
+            double d0[DM], d1[DM];
 #pragma unroll
-            for (int jj = 0; jj < DM; ++jj) dd[jj] = S.xd[s][h * DM * 128 + jj * 128 + rw] - mk[jj];
-            double q = 0.0;
+            for (int jj = 0; jj < DM; ++jj) {
+                d0[jj] = S.xd[s][(e0 >> 7) * DM * 128 + jj * 128 + (e0 & 127)] - mk[jj];
+                d1[jj] = S.xd[s][(e1 >> 7) * DM * 128 + jj * 128 + (e1 & 127)] - mk[jj];
+            }
+            double q0 = 0.0, q1 = 0.0;
 #pragma unroll
             for (int r = 0; r < DM; ++r) {
-                double a = 0.0;
+                double a0 = 0.0, a1 = 0.0;
 #pragma unroll
                 for (int jj = 0; jj <= r; jj += 2) {  // W rows read as double2 (upper triangle is zero)
                     const double2 wv = *reinterpret_cast<const double2*>(Wk + r * DM + jj);
-                    a = fma(wv.x, dd[jj], a);
-                    if (jj + 1 <= r) a = fma(wv.y, dd[jj + 1], a);
+                    a0 = fma(wv.x, d0[jj], a0);
+                    a1 = fma(wv.x, d1[jj], a1);
+                    if (jj + 1 <= r) {
+                        a0 = fma(wv.y, d0[jj + 1], a0);
+                        a1 = fma(wv.y, d1[jj + 1], a1);
+                    }
                 }
-                q = fma(a, a, q);
+                q0 = fma(a0, a0, q0);
+                q1 = fma(a1, a1, q1);
             }
-            S.lnv[k * TT + ev] = S.ln64[k] - 0.5 * q;
+            S.lnv[k * TT + e0] = S.ln64[k] - 0.5 * q0;
+            if (e1r != 0xFFFF) S.lnv[k * TT + e1] = S.ln64[k] - 0.5 * q1;
         }
         __syncthreads();
         double mm = -INFINITY, bb = -INFINITY;
