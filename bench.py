@@ -276,8 +276,10 @@ def run_ours(args):
                  if ctx.precision == "mixed" and ek.startswith("w") else
                  "k_em_tc (tcgen05 3xTF32 whitening + FP32/FP64 M-step)" if ctx.precision == "mixed" and ek == "tc" else
                  "k_em_fast<16> (SIMT FP32)" if ctx.precision == "mixed" else "k_em_team<16,2> (FP64)")
-    sc_kernel = ("k_score_tc (tcgen05 3xTF32 + FP64 candidate refine)" if ctx.precision == "mixed" and
-                 os.environ.get("ES_SCORE_KERNEL", "tc") != "simt" else
+    sk = os.environ.get("ES_SCORE_KERNEL", "mma")
+    sc_kernel = ("k_score_mma (tcgen05 3xfp16 whitening + FP64 candidate refinement, 3 warpgroups)"
+                 if ctx.precision == "mixed" and sk.startswith("m") else
+                 "k_score_tc (tcgen05 3xTF32 + FP64 candidate refine)" if ctx.precision == "mixed" and sk == "tc" else
                  "k_score_fast<16> (FP32 + FP64 refine)" if ctx.precision == "mixed" else "k_score_team<16> (FP64)")
     it_s = args.steps / (em_ms_max / 1e3)
     bytes_iter = n_global * D * 8

@@ -109,6 +109,12 @@ bool make_event_tmap(CUtensorMap* map, const double* X, int64_t n, int64_t ld, i
 bool score_tc_supported(int D, int K, const ScoreOut& o);
 void launch_score_tc(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model, const double* center,
                      const ScoreOut& o, double* blocksum, int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
+// Fused-pipeline scoring pass (es_score_mma.cu), the default for D <= 16, K <= 8:
+// center_host / xs as for launch_em_mma (x^ = (x - c) xs, xs a power of two).
+bool score_mma_enabled(int D, int K, const ScoreOut& o);
+void launch_score_mma(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model, const double* center,
+                      const double* center_host, double xs, const ScoreOut& o, double* blocksum, int num_sms,
+                      int* nblk, cudaStream_t s, LaunchStats& ls);
 bool score_fast_supported(int D, int K, const ScoreOut& o);
 void launch_score_fast(const double* X, int64_t n, int64_t ld, int D, int K, const double* model,
                        const double* center, const ScoreOut& o, double* blocksum, int num_sms, int* nblk,

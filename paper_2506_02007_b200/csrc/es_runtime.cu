@@ -173,6 +173,8 @@ struct es_ctx {
     LaunchStats ls;
     DevBuf partial, stats_local, stats_all, model, model_backup, status, scratch, scratch2, scratch3, out_scratch,
         hist, xbuf, o1, o2, o3, o4, o5, kpp, center;
+    std::vector<double> center_host;  // host copy of `center` (scoring kernels' FP64 centre)
+    double center_xs = 1.0;           // power of two bringing the model's span into (8, 16]
     int precision = 0;  // 0 = mixed (FP32 whitening, FP64 statistics), 1 = strict FP64
     IterStatus* h_status = nullptr;  // pinned
     std::vector<double> hbuf;
@@ -432,6 +434,15 @@ double* model_for(es_ctx* c, const es_gmm_params* p, int D) {
         for (int j = 0; j < D; ++j) cen[j] += (z > 0 ? p->weights[k] / z : 1.0 / p->K) * p->means[(size_t)k * D + j];
     double* dc = c->center.as<double>(D);
     CU(cudaMemcpyAsync(dc, cen.data(), D * 8, cudaMemcpyHostToDevice, c->stream));
+    // x^ = (x - c) xs for the tcgen05 scorer: the model's span (means +- 8 sigma) maps into
+    // (8, 16]; events further out are refined entirely in FP64 by the kernel
+    double span = 0.0;
+    for (int k = 0; k < p->K; ++k)
+        for (int j = 0; j < D; ++j)
+            span = std::max(span, std::fabs(p->means[(size_t)k * D + j] - cen[j]) +
+                                      8.0 * std::sqrt(std::max(p->covariances[(size_t)k * D * D + j * D + j], 0.0)));
+    c->center_host = cen;
+    c->center_xs = span > 0.0 && std::isfinite(span) ? std::ldexp(1.0, 4 - (int)std::ceil(std::log2(span))) : 1.0;
     return m;
 }
 
@@ -454,8 +465,12 @@ struct Out {
 
 // Scoring launch: mixed-precision kernel when supported, FP64 team kernel otherwise.
 void score_launch(es_ctx* c, const double* X, int64_t n, int64_t ld, int D, int K, const double* dmodel,
-                  const double* center, const ScoreOut& o, double* bs, int* nblk, const CUtensorMap* xmap = nullptr) {
-    if (c->precision == 0 && center && xmap && score_tc_supported(D, K, o))
+                  const double* center, const double* center_host, double xs, const ScoreOut& o, double* bs,
+                  int* nblk, const CUtensorMap* xmap = nullptr) {
+    if (c->precision == 0 && center && center_host && xmap && score_mma_enabled(D, K, o))
+        launch_score_mma(xmap, n, D, K, dmodel, center, center_host, xs, o, bs, c->num_sms, nblk, c->stream,
+                         c->ls);
+    else if (c->precision == 0 && center && xmap && score_tc_supported(D, K, o))
         launch_score_tc(xmap, n, D, K, dmodel, center, o, bs, c->num_sms, nblk, c->stream, c->ls);
     else if (c->precision == 0 && center && score_fast_supported(D, K, o))
         launch_score_fast(X, n, ld, D, K, dmodel, center, o, bs, c->num_sms, nblk, c->stream, c->ls);
@@ -465,14 +480,15 @@ void score_launch(es_ctx* c, const double* X, int64_t n, int64_t ld, int D, int 
 
 size_t score_blocks(es_ctx* c, int D, int K) { return (size_t)2 * std::max(score_grid(D, K, c->num_sms), 2 * c->num_sms) + 2; }
 
-double run_score(es_ctx* c, es_dataset* ds, const double* dmodel, int K, ScoreOut o, const double* center) {
+double run_score(es_ctx* c, es_dataset* ds, const double* dmodel, int K, ScoreOut o, const double* center,
+                 const double* center_host, double xs) {
     const int D = ds->D;
     double* bs = c->scratch.as<double>(score_blocks(c, D, K));
     double loc = 0.0;
     if (ds->n_local > 0) {
         int nblk = 0;
         c->t_begin();
-        score_launch(c, ds->X, ds->n_local, ds->ld, D, K, dmodel, center, o, bs, &nblk,
+        score_launch(c, ds->X, ds->n_local, ds->ld, D, K, dmodel, center, center_host, xs, o, bs, &nblk,
                      ds->has_xmap ? &ds->xmap : nullptr);
         c->t_end(c->score_ms, c->score_launches);
         double* red = c->scratch2.as<double>(2);
@@ -1088,7 +1104,7 @@ int es_gmm_em_end(es_em_state* st, es_gmm_params* out, es_fit_report* rep, doubl
         const int K = st->K, D = st->D;
         double* dmodel = c->model.as<double>(mstride(K, D));
         double final_ll = st->last;
-        if (!st->converged) final_ll = run_score(c, st->ds, dmodel, K, ScoreOut{}, st->dcenter.as<double>(D));
+        if (!st->converged) final_ll = run_score(c, st->ds, dmodel, K, ScoreOut{}, st->dcenter.as<double>(D), st->mean.data(), st->xs);
         if (out) {
             if (out->K != K || out->D != D) fail(ES_ERR_DATA, "DimensionMismatch", "output params shape");
             ModelView mv{K, D, dmodel};
@@ -1140,7 +1156,7 @@ int es_gmm_score(es_ctx* c, es_dataset* ds, const es_gmm_params* p, double* ll, 
         o.best_ld = o_bl.dev;
         o.predict = o_pr.dev;
         o.best_k = o_bk.dev;
-        const double tot = run_score(c, ds, m, p->K, o, c->center.as<double>(ds->D));
+        const double tot = run_score(c, ds, m, p->K, o, c->center.as<double>(ds->D), c->center_host.data(), c->center_xs);
         o_ll.finish(c->stream);
         o_bl.finish(c->stream);
         o_pr.finish(c->stream);
@@ -1157,7 +1173,7 @@ int es_gmm_responsibilities(es_ctx* c, es_dataset* ds, const es_gmm_params* p, d
         Out<double> o_g(gamma, (size_t)ds->n_local * p->K, c->o1);
         ScoreOut o;
         o.gamma = o_g.dev;
-        run_score(c, ds, m, p->K, o, c->center.as<double>(ds->D));
+        run_score(c, ds, m, p->K, o, c->center.as<double>(ds->D), c->center_host.data(), c->center_xs);
         o_g.finish(c->stream);
         c->sync();
     });
@@ -1222,7 +1238,7 @@ int es_gmm_detect(es_ctx* c, es_dataset* ds, const es_gmm_params* p, double log_
         o.best_ld = o_bl.dev;
         o.log_delta = log_delta;
         o.mode = mode;
-        run_score(c, ds, m, p->K, o, c->center.as<double>(ds->D));
+        run_score(c, ds, m, p->K, o, c->center.as<double>(ds->D), c->center_host.data(), c->center_xs);
         int64_t* cnt = c->scratch2.as<int64_t>((n + 4095) / 4096 + 2);
         int64_t* dcount = cnt + (n + 4095) / 4096 + 1;
         launch_compact(dflags, n, ds->row_offset, cnt, o_idx.dev, dcount, c->stream, c->ls);
@@ -1261,7 +1277,8 @@ int es_gmm_calibrate(es_ctx* c, es_dataset* ds, const es_gmm_params* p, int64_t 
             else o.best_ld = keys;
             int nblk = 0;
             double* bs = c->scratch.as<double>(score_blocks(c, ds->D, p->K));
-            score_launch(c, ds->X, nloc, ds->ld, ds->D, p->K, m, c->center.as<double>(ds->D), o, bs, &nblk,
+            score_launch(c, ds->X, nloc, ds->ld, ds->D, p->K, m, c->center.as<double>(ds->D), c->center_host.data(),
+                         c->center_xs, o, bs, &nblk,
                          ds->has_xmap ? &ds->xmap : nullptr);
             c->check_launch();
         }
