@@ -824,8 +824,111 @@ void launch_em_pass(const double* X, int64_t n, int64_t ld, int D, int K, const 
     ++ls.launches;
 }
 
+// Unit-weight statistics about `center` for D <= 16 on the FP64 tensor pipe: per warp, a
+// contiguous event range; per 4 events one mma.sync m8n8k4 f64 k-step of the Gram
+// G = D^T D (D = centred rows), blocks (0,0), (0,1), (1,1) of the 16 x 16 matrix; the A and
+// B fragments are the same loaded values (thread t: feature t/4 + 8 m, event t%4).  Four
+// k-steps in flight per warp (independent accumulators).  FP64 products and sums.
+__global__ void __launch_bounds__(256) k_unit_gram(const double* __restrict__ X, int64_t n, int64_t ld, int D,
+                                                    const double* __restrict__ center, double* __restrict__ partial) {
+    constexpr int U = 4;
+    __shared__ double red[8][16 * 16 + 16];
+    const int t = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * 8 + warp, nw = (int64_t)gridDim.x * 8;
+    const int64_t chunk = ((n + nw - 1) / nw + 4 * U - 1) / (4 * U) * (4 * U);
+    const int64_t e0 = gw * chunk, e1 = min(n, e0 + chunk);
+    const int f0 = t >> 2, f1 = f0 + 8, ev = t & 3;
+    const double c0 = f0 < D ? center[f0] : 0.0, c1 = f1 < D ? center[f1] : 0.0;
+    const double* x0 = X + (int64_t)f0 * ld;
+    const double* x1 = X + (int64_t)f1 * ld;
+    double acc[U][3][2];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) acc[u][b][0] = acc[u][b][1] = 0.0;
+    double s0 = 0.0, s1 = 0.0;
+    for (int64_t e = e0; e < e1; e += 4 * U) {
+        double d0[U], d1[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = e + 4 * u + ev;
+            const bool ok = i < e1;
+            d0[u] = (ok && f0 < D) ? __ldg(x0 + i) - c0 : 0.0;
+            d1[u] = (ok && f1 < D) ? __ldg(x1 + i) - c1 : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            s0 += d0[u];
+            s1 += d1[u];
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[u][0][0]), "+d"(acc[u][0][1]) : "d"(d0[u]), "d"(d0[u]));
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[u][1][0]), "+d"(acc[u][1][1]) : "d"(d0[u]), "d"(d1[u]));
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[u][2][0]), "+d"(acc[u][2][1]) : "d"(d1[u]), "d"(d1[u]));
+        }
+    }
+    // C fragment: row f0 (+8), columns 2 (t & 3) + {0, 1} (+8); fixed-order sums
+    double* r = red[warp];
+    const int cn = 2 * (t & 3);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        double g00 = 0.0, g01 = 0.0, g11 = 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            g00 += acc[u][0][h];
+            g01 += acc[u][1][h];
+            g11 += acc[u][2][h];
+        }
+        r[f0 * 16 + cn + h] = g00;
+        r[f0 * 16 + 8 + cn + h] = g01;
+        r[(8 + cn + h) * 16 + f0] = g01;  // (1,0) = (0,1)^T
+        r[f1 * 16 + 8 + cn + h] = g11;
+    }
+    s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
+    s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
+    if ((t & 3) == 0) {
+        r[256 + f0] = s0;
+        r[256 + f1] = s1;
+    }
+    __syncthreads();
+    // block partial: [N | s1[D] | s2 packed upper | logL = 0]
+    const int SK = stat_k(D);
+    double* out = partial + (int64_t)blockIdx.x * (SK + 1);
+    for (int j = threadIdx.x; j < SK + 1; j += blockDim.x) {
+        double v = 0.0;
+        if (j == 0) {
+            for (int w = 0; w < 8; ++w) {
+                const int64_t a = ((int64_t)blockIdx.x * 8 + w) * chunk;
+                const int64_t lo = a < n ? a : n, hi = a + chunk < n ? a + chunk : n;
+                v += (double)(hi - lo);
+            }
+        } else if (j <= D) {
+            for (int w = 0; w < 8; ++w) v += red[w][256 + j - 1];
+        } else if (j < SK) {
+            int pp = j - 1 - D, a = 0;
+            while (pp >= D - a) {
+                pp -= D - a;
+                ++a;
+            }
+            const int b = a + pp;
+            for (int w = 0; w < 8; ++w) v += red[w][a * 16 + b];
+        }
+        out[j] = v;
+    }
+}
+
 void launch_unit_stats(const double* X, int64_t n, int64_t ld, int D, const double* center, double* partial,
                        int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls) {
+    if (D <= 16) {
+        const int grid = num_sms * 4;
+        *nblk = grid;
+        k_unit_gram<<<grid, 256, 0, s>>>(X, n, ld, D, center, partial);
+        ++ls.launches;
+        return;
+    }
     const int grid = num_sms * 2;
     *nblk = grid;
     const int T = generic_tile(D, 1);
