@@ -99,6 +99,9 @@ bool em_mma_enabled();
 // Record precision: npass 2 (fp16 hi + lo records) or 1 (single fp16 record, used when
 // every component has >= kOnePassMinNk events); ES_EM_MMA_PASSES=1|2 overrides.
 constexpr double kOnePassMinNk = 1048576.0;
+// Mixed-precision (tcgen05 E-step) EM passes run only when every component has at least
+// this many events; below, the iteration uses the strict FP64 kernel.
+constexpr double kMixedMinNk = 16384.0;
 int em_mma_passes();
 void launch_em_mma(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model, const double* center,
                    const double* center_host, double xs, int npass, double* partial, int num_sms, int* nblk,

@@ -664,6 +664,13 @@ void em_begin(es_em_state* st, const es_gmm_params* init) {
     em_init_model(st, init, dsx);
 }
 
+// The mixed-precision EM passes (tcgen05 E-step) need enough events per component for
+// the per-event rounding of the whitening to average out: below
+// kMixedMinNk events in some component the iteration runs on the strict FP64 kernel.
+bool mixed_em(es_ctx* c, const es_em_state* st) {
+    return c->precision == 0 && em_fast_supported(st->D, st->K) && st->min_nk >= kMixedMinNk;
+}
+
 // One EM iteration; returns true when the loop must stop.
 bool em_iterate(es_em_state* st) {
     es_ctx* c = st->ctx;
@@ -688,7 +695,8 @@ bool em_iterate(es_em_state* st) {
         double* part = c->partial.as<double>((size_t)std::max(em_grid(D, K, c->num_sms), c->num_sms) * NE1);
         c->t_begin();
         bool wh = true, wh_mma = false;
-        if (c->precision == 0 && em_fast_supported(D, K)) {
+        st->last_npass = 0;
+        if (mixed_em(c, st)) {
             if (em_mma_enabled() && ds->has_xmap) {
                 const int np = st->min_nk >= kOnePassMinNk ? 1 : 2;
                 launch_em_mma(&ds->xmap, ds->n_local, D, K, dmodel, st->dcenter.as<double>(D), st->mean.data(),
@@ -717,7 +725,7 @@ bool em_iterate(es_em_state* st) {
         // an empty shard must announce the same statistics format as the others
         if (is_diag(st))
             whitened = 2;
-        else if (c->precision == 0 && em_fast_supported(D, K))
+        else if (mixed_em(c, st))
             whitened = em_mma_enabled() ? 3 : 0;
         else
             whitened = em_path(D, K) != EmPath::Generic ? 1 : 0;

@@ -263,11 +263,26 @@ def test_full_size_one_pass_records_vs_fp64(es):
 
 def test_two_pass_records_small_components(es, oracle):
     """Below 2^20 events per component the fused pass switches to hi + lo records."""
-    ds, X = syn(es, oracle, 1 << 18, 16, 8)
-    em = es.EM(ds, 8, init="random", tol=0.0, max_iter=8, seed=7)
-    em.step(8)
+    ds, X = syn(es, oracle, 1 << 20, 16, 8)
+    em = es.EM(ds, 8, init="random", tol=0.0, max_iter=6, seed=7)
+    em.step(6)
     assert em.record_passes == 2
     m = em.finish()
     em.close()
-    pi, mu, cov, rep = oracle.fit_em(X, 8, init="random", tol=0.0, max_iter=8, seed=7)
+    pi, mu, cov, rep = oracle.fit_em(X, 8, init="random", tol=0.0, max_iter=6, seed=7)
     assert_params(m, pi, mu, cov)
+
+
+def test_small_components_use_strict_passes(es, oracle):
+    """With fewer than 2^14 events in some component the iteration runs on the strict FP64
+    kernel (the tensor-core whitening's per-event rounding would not average out)."""
+    ds, X = syn(es, oracle, 1000, 16, 8)
+    em = es.EM(ds, 8, init="random", tol=0.0, max_iter=10, seed=7)
+    em.step(10)
+    assert em.record_passes == 0
+    m = em.finish()
+    em.close()
+    pi, mu, cov, rep = oracle.fit_em(X, 8, init="random", tol=0.0, max_iter=10, seed=7)
+    assert_params(m, pi, mu, cov)
+    assert np.all(np.abs(m.fit_report.per_iteration_log_likelihoods - rep["per_iteration_log_likelihoods"])
+                  <= LL_TOL * np.abs(rep["per_iteration_log_likelihoods"]))
