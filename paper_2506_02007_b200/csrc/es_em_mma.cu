@@ -155,11 +155,20 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
             cst[k] = S.cst[k];
             hq[k] = S.hq[k];
         }
-        double g2[DM], g1 = 0.0, nk[KMAX], llacc = 0.0;
+        // statistics in compensated FP32 pairs (hi, lo): Gram row, first moment, N_k; logL in FP64
+        uint64_t g2h[DM / 2], g2l[DM / 2], nkh[KMAX / 2], nkl[KMAX / 2];
+        float g1h = 0.f, g1l = 0.f;
+        double llacc = 0.0;
 #pragma unroll
-        for (int b = 0; b < DM; ++b) g2[b] = 0.0;
+        for (int b = 0; b < DM / 2; ++b) g2h[b] = g2l[b] = 0;
 #pragma unroll
-        for (int k = 0; k < KMAX; ++k) nk[k] = 0.0;
+        for (int k = 0; k < KMAX / 2; ++k) nkh[k] = nkl[k] = 0;
+        auto g2v = [&](int b) { return cval(g2h[b >> 1], g2l[b >> 1], b & 1); };
+        auto set2 = [&](uint64_t& hi, uint64_t& lo, double a, double b) {
+            const float ah = (float)a, bh = (float)b;
+            hi = pack2(ah, bh);
+            lo = pack2((float)(a - (double)ah), (float)(b - (double)bh));
+        };
 
         auto flush = [&](int64_t jj) {  // Gram of this WG's local tile jj -> FP64
             mbar_wait(su32(&S.mdone[w]), (uint32_t)(jj & 1));
@@ -178,15 +187,16 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
                 m1 = hsel ? f1 : f0;
             }
 #pragma unroll
-            for (int b = 0; b < DM; ++b) g2[b] += (double)(hsel ? v[16 + b] : v[b]);
-            g1 += (double)m1;
+            for (int b = 0; b < DM; b += 2)
+                cacc2(g2h[b / 2], g2l[b / 2], hsel ? pack2(v[16 + b], v[17 + b]) : pack2(v[b], v[b + 1]));
+            cacc(g1h, g1l, m1);
             tc_fence_before();
         };
         // N_k of this WG (fixed-order reduction) -> S.ntot[w]
         auto wg_counts = [&]() {
 #pragma unroll
             for (int k = 0; k < KMAX; ++k) {
-                const double v = warp_sum(nk[k]);
+                const double v = warp_sum(cval(nkh[k >> 1], nkl[k >> 1], k & 1));
                 if (lane == 0) S.wred[warp][k] = v;
             }
             named_sync(3 + w, 128);
@@ -205,6 +215,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
         auto recentre = [&](bool back) {
             wg_counts();
             const double N = S.ntot[w][kk];
+            double g1 = (double)g1h + (double)g1l;
             double d = 0.0;
             if (back) {
                 d = -S.shift[w][p];
@@ -217,11 +228,18 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
             S.s1x[w][p] = g1;
             named_sync(3 + w, 128);
 #pragma unroll
-            for (int bb = 0; bb < DM; ++bb) {
-                const double db = S.dl[w][kk * DM + bb], sb = S.s1x[w][kk * DM + bb];
-                g2[bb] += fma(N * d, db, -fma(g1, db, d * sb));
+            for (int bb = 0; bb < DM; bb += 2) {
+                double nv[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const double db = S.dl[w][kk * DM + bb + h], sb = S.s1x[w][kk * DM + bb + h];
+                    nv[h] = g2v(bb + h) + fma(N * d, db, -fma(g1, db, d * sb));
+                }
+                set2(g2h[bb / 2], g2l[bb / 2], nv[0], nv[1]);
             }
             g1 = fma(-N, d, g1);
+            g1h = (float)g1;
+            g1l = (float)(g1 - (double)g1h);
             if (!back) {
                 S.nmu[w][p] = -(float)(-(double)S.nmu[w][p] + d);
                 S.shift[w][p] += d;
@@ -296,7 +314,11 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
 #pragma unroll
             for (int k = 0; k < KMAX; ++k) {
                 sg[k] = valid ? ex2((wk[k] - ll) * 0.7213475204444817f) : 0.f;
-                nk[k] += (double)(sg[k] * sg[k]);
+            }
+#pragma unroll
+            for (int k = 0; k < KMAX; k += 2) {
+                const uint64_t s2v = pack2(sg[k], sg[k + 1]);
+                cacc2(nkh[k / 2], nkl[k / 2], mul2(s2v, s2v));
             }
             if (valid) llacc += (double)ll;
             // ---- records (buffers w are free once the Gram of the previous tile completed)
@@ -375,7 +397,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
         // Gram, sym(P) = (P + P^T) / 2.  The record buffers are free now (scratch).
 #pragma unroll
         for (int k = 0; k < KMAX; ++k) {
-            const double v = warp_sum(nk[k]);
+            const double v = warp_sum(cval(nkh[k >> 1], nkl[k >> 1], k & 1));
             if (lane == 0) S.wred[warp][k] = v;
         }
         {
@@ -385,8 +407,8 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
         double* rows = reinterpret_cast<double*>(&S.rech[0][0]);  // [2][128][17]
         named_sync(5, 256);  // both WGs drained: no Gram still reads the record buffers
 #pragma unroll
-        for (int b = 0; b < DM; ++b) rows[(w * TM + p) * (DM + 1) + b] = g2[b];
-        rows[(w * TM + p) * (DM + 1) + DM] = g1;
+        for (int b = 0; b < DM; ++b) rows[(w * TM + p) * (DM + 1) + b] = g2v(b);
+        rows[(w * TM + p) * (DM + 1) + DM] = (double)g1h + (double)g1l;
         named_sync(5, 256);
         if (w == 0) {
             const int SK = stat_k(D), NE = K * SK;

@@ -124,6 +124,25 @@ __device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
     asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
     return r;
 }
+// Compensated FP32 accumulation of two lanes, (hi, lo) += x (Fast2Sum: the rounding error
+// of hi + x is exact while |hi| >= |x|, which holds once a few tiles are in): ~44-bit
+// accumulation on the FP32 pipe instead of F2F + DADD on the much narrower FP64 pipe.
+__device__ __forceinline__ void cacc2(uint64_t& hi, uint64_t& lo, uint64_t x) {
+    const uint64_t s2 = add2(hi, x);
+    lo = add2(lo, sub2(x, sub2(s2, hi)));
+    hi = s2;
+}
+__device__ __forceinline__ void cacc(float& hi, float& lo, float x) {
+    const float s = hi + x;
+    lo += x - (s - hi);
+    hi = s;
+}
+__device__ __forceinline__ double cval(uint64_t hi, uint64_t lo, int h) {
+    float a, b, c, d;
+    unpack2(hi, a, b);
+    unpack2(lo, c, d);
+    return h ? (double)b + (double)d : (double)a + (double)c;
+}
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
