@@ -157,8 +157,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
         }
         // statistics in compensated FP32 pairs (hi, lo): Gram row, first moment, N_k; logL in FP64
         uint64_t g2h[DM / 2], g2l[DM / 2], nkh[KMAX / 2], nkl[KMAX / 2];
-        float g1h = 0.f, g1l = 0.f;
-        double llacc = 0.0;
+        float g1h = 0.f, g1l = 0.f, llh = 0.f, lll = 0.f;
 #pragma unroll
         for (int b = 0; b < DM / 2; ++b) g2h[b] = g2l[b] = 0;
 #pragma unroll
@@ -320,7 +319,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
                 const uint64_t s2v = pack2(sg[k], sg[k + 1]);
                 cacc2(nkh[k / 2], nkl[k / 2], mul2(s2v, s2v));
             }
-            if (valid) llacc += (double)ll;
+            if (valid) cacc(llh, lll, ll);
             // ---- records (buffers w are free once the Gram of the previous tile completed)
             if (pend) {
                 flush(jj - 1);
@@ -401,7 +400,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
             if (lane == 0) S.wred[warp][k] = v;
         }
         {
-            const double v = warp_sum(llacc);
+            const double v = warp_sum((double)llh + (double)lll);
             if (lane == 0) S.wred[warp][KMAX] = v;
         }
         double* rows = reinterpret_cast<double*>(&S.rech[0][0]);  // [2][128][17]
