@@ -79,11 +79,11 @@ struct Smem {
 
 }  // namespace
 
-template <int NPASS>
+template <int NPASS, bool F32>
 __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUtensorMap xmap, int64_t n, int D,
                                                      int K, const double* __restrict__ model,
                                                      const double* __restrict__ center, double xs,
-                                                     const __grid_constant__ NegCx ncx,
+                                                     const __grid_constant__ NegCx ncx, const float2 xsf_c,
                                                      double* __restrict__ partial) {
     using Sm = Smem<NPASS>;
     constexpr int XS = Sm::XS;
@@ -256,8 +256,14 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
             uint32_t hw[DM / 2], lw[DM / 2];
 #pragma unroll
             for (int f = 0; f < DM; f += 2) {
-                const float v0 = (float)fma(S.xd[s][f * TM + p], xs, ncx.v[f]);
-                const float v1 = (float)fma(S.xd[s][(f + 1) * TM + p], xs, ncx.v[f + 1]);
+                float v0, v1;
+                if (F32) {  // FP32 pipe: x within 4x of its spread about c (see launch_em_mma)
+                    v0 = fmaf(__double2float_rn(S.xd[s][f * TM + p]), xsf_c.x, (float)ncx.v[f]);
+                    v1 = fmaf(__double2float_rn(S.xd[s][(f + 1) * TM + p]), xsf_c.x, (float)ncx.v[f + 1]);
+                } else {
+                    v0 = (float)fma(S.xd[s][f * TM + p], xs, ncx.v[f]);
+                    v1 = (float)fma(S.xd[s][(f + 1) * TM + p], xs, ncx.v[f + 1]);
+                }
                 x2[f / 2] = pack2(v0, v1);
                 const uint32_t h = pack_h2(v0, v1);
                 const float2 hf = __half22float2(u2h(h));
@@ -528,32 +534,43 @@ int em_mma_passes() {
     return v;
 }
 
-template <int NPASS>
+template <int NPASS, bool F32>
 static void launch_npass(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model,
                          const double* center, double xs, const NegCx& ncx, double* partial, int grid,
                          cudaStream_t s) {
     const size_t smem = sizeof(Smem<NPASS>) + 128;
     static bool a = false;
     if (!a) {
-        cudaFuncSetAttribute(k_em_mma<NPASS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_em_mma<NPASS, F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         a = true;
     }
-    k_em_mma<NPASS><<<grid, NTHR, smem, s>>>(*xmap, n, D, K, model, center, xs, ncx, partial);
+    k_em_mma<NPASS, F32><<<grid, NTHR, smem, s>>>(*xmap, n, D, K, model, center, xs, ncx,
+                                                   make_float2((float)xs, 0.f), partial);
 }
 
 void launch_em_mma(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model, const double* center,
-                   const double* center_host, double xs, int npass, double* partial, int num_sms, int* nblk,
-                   cudaStream_t s, LaunchStats& ls) {
+                   const double* center_host, double xs, bool f32conv, int npass, double* partial, int num_sms,
+                   int* nblk, cudaStream_t s, LaunchStats& ls) {
     NegCx ncx{};
     for (int j = 0; j < D && j < DM; ++j) ncx.v[j] = -center_host[j] * xs;
+    static int allow = -1;
+    if (allow < 0) {
+        const char* e = getenv("ES_EM_F32CONV");
+        allow = (e && e[0] == '0') ? 0 : 1;
+    }
+    f32conv = f32conv && allow;
     const int64_t ntiles = (n + TM - 1) / TM;
     const int grid = (int)std::min<int64_t>(num_sms, std::max<int64_t>(ntiles, 1));
     *nblk = grid;
     if (em_mma_passes() != 0) npass = em_mma_passes();
-    if (npass == 1)
-        launch_npass<1>(xmap, n, D, K, model, center, xs, ncx, partial, grid, s);
+    if (npass == 1 && f32conv)
+        launch_npass<1, true>(xmap, n, D, K, model, center, xs, ncx, partial, grid, s);
+    else if (npass == 1)
+        launch_npass<1, false>(xmap, n, D, K, model, center, xs, ncx, partial, grid, s);
+    else if (f32conv)
+        launch_npass<2, true>(xmap, n, D, K, model, center, xs, ncx, partial, grid, s);
     else
-        launch_npass<2>(xmap, n, D, K, model, center, xs, ncx, partial, grid, s);
+        launch_npass<2, false>(xmap, n, D, K, model, center, xs, ncx, partial, grid, s);
     ++ls.launches;
 }
 

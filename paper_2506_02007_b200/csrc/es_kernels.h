@@ -103,9 +103,11 @@ constexpr double kOnePassMinNk = 1048576.0;
 // this many events; below, the iteration uses the strict FP64 kernel.
 constexpr double kMixedMinNk = 16384.0;
 int em_mma_passes();
+// f32conv: max|x| <= 4 max|x - c| over the data, so x^ = (x - c) xs may be formed on the FP32
+// pipe (error <= 2^-24 * 64 in x^ units) instead of an FP64 fma per value (ES_EM_F32CONV=0 off).
 void launch_em_mma(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model, const double* center,
-                   const double* center_host, double xs, int npass, double* partial, int num_sms, int* nblk,
-                   cudaStream_t s, LaunchStats& ls);
+                   const double* center_host, double xs, bool f32conv, int npass, double* partial, int num_sms,
+                   int* nblk, cudaStream_t s, LaunchStats& ls);
 // Builds that tensor map (driver entry point resolved through the runtime).
 bool make_event_tmap(CUtensorMap* map, const double* X, int64_t n, int64_t ld, int D);
 // tcgen05 scoring pass (es_score_tc.cu); ES_SCORE_KERNEL=simt selects k_score_fast.

@@ -274,6 +274,7 @@ struct es_em_state {
     std::vector<double> S;  // data covariance (D x D)
     std::vector<double> mean;  // data mean: FP64 centre of the mixed-precision path
     double xs = 1.0;           // power of two bringing max|x - mean| into (8, 16] (k_em_mma operand scale)
+    bool f32conv = false;      // max|x| <= 4 max|x - mean|: x^ may be formed on the FP32 pipe
     double min_nk = 0.0;       // min_k N_k of the current model (global), selects k_em_mma's record precision
     int last_npass = 0;        // record precision of the last k_em_mma pass (0: other kernel)
     DevBuf dcenter;
@@ -654,9 +655,13 @@ void em_begin(es_em_state* st, const es_gmm_params* init) {
     st->S = dsx.S;
     st->mean = dsx.mean;
     {
-        double span = 0.0;
-        for (int j = 0; j < D; ++j) span = std::max(span, std::max(dsx.mx[j] - dsx.mean[j], dsx.mean[j] - dsx.mn[j]));
+        double span = 0.0, mag = 0.0;
+        for (int j = 0; j < D; ++j) {
+            span = std::max(span, std::max(dsx.mx[j] - dsx.mean[j], dsx.mean[j] - dsx.mn[j]));
+            mag = std::max(mag, std::max(std::fabs(dsx.mx[j]), std::fabs(dsx.mn[j])));
+        }
         st->xs = span > 0.0 ? std::ldexp(1.0, 4 - (int)std::ceil(std::log2(span))) : 1.0;
+        st->f32conv = span > 0.0 && mag <= 4.0 * span && mag < 1e30;
     }
     CU(cudaMemcpyAsync(st->dcenter.as<double>(D), dsx.mean.data(), D * 8, cudaMemcpyHostToDevice, c->stream));
     st->reg = st->opts.reg < 0 ? default_reg(dsx.S, D) : st->opts.reg;
@@ -700,7 +705,7 @@ bool em_iterate(es_em_state* st) {
             if (em_mma_enabled() && ds->has_xmap) {
                 const int np = st->min_nk >= kOnePassMinNk ? 1 : 2;
                 launch_em_mma(&ds->xmap, ds->n_local, D, K, dmodel, st->dcenter.as<double>(D), st->mean.data(),
-                              st->xs, np, part, c->num_sms, &nblk, c->stream, c->ls);
+                              st->xs, st->f32conv, np, part, c->num_sms, &nblk, c->stream, c->ls);
                 st->last_npass = em_mma_passes() ? em_mma_passes() : np;
                 wh_mma = true;
             } else if (em_ws_enabled() && ds->has_xmap)
