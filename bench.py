@@ -325,7 +325,7 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override N (debug only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--traffic", type=float, default=8590243000.0 + 6040576.0,
+    ap.add_argument("--traffic", type=float, default=8590171000.0 + 8156928.0,
                     help="dram bytes per EM launch from the committed ncu --set full capture (profiles/)")
     ap.add_argument("--traffic-note", default="dram__bytes_read.sum + dram__bytes_write.sum of k_em_mma<1> at N=2^26, "
                                               "profiles/r01_k_em_mma1_ncu_summary.txt")
