@@ -46,4 +46,19 @@ double calibrate_threshold(const GmmModel& model, const FeatureMatrix& X_train, 
 std::pair<double, double> calibrate_threshold_log(const GmmModel& model, const FeatureMatrix& X_train, double q,
                                                   DetectMode mode = DetectMode::Component);
 
+struct PipelineResult {               // run_pipeline outputs (EvalSummary: eval-bench, not built)
+    DetectionReport report;           // over ALL events; report.model is in standardized space
+    FeatureMatrix::Standardization standardization;  // per column (mean, stddev) of the train split
+    std::int64_t n_train = 0;
+};
+
+/// run_pipeline over a time-ordered feature matrix: the first
+/// floor(train_window * N) rows are the training split; columns are z-scored with its
+/// mean and population stddev (zero-variance columns centred only) when `standardize`;
+/// a cfg.K-component GMM is fitted there; delta = cfg.quantile_q-quantile of the training
+/// densities (or cfg.delta); every event is scored per detect.  Errors: InsufficientTraining
+/// (training split < 10 K), plus the component ops' errors.
+PipelineResult run_pipeline(const FeatureMatrix& X, const DetectorConfig& cfg, const FitOptions& opts = {},
+                            bool standardize = true);
+
 }  // namespace eventscope

@@ -26,7 +26,8 @@ struct FeatureMatrix {
     int dim = 0;
     std::vector<double> data;                 // rows * dim, row-major
     std::vector<std::string> feature_names;   // dim entries (optional)
-    std::vector<std::pair<double, double>> standardization;  // per column (mean, stddev), optional
+    using Standardization = std::vector<std::pair<double, double>>;
+    Standardization standardization;          // per column (mean, stddev), optional
     std::vector<std::int64_t> event_index;    // back-references (optional)
 };
 

@@ -17,6 +17,7 @@
  *   es_gmm_detect            <- detect
  *   es_gmm_calibrate         <- calibrate_threshold
  *   es_gmm_select_k_bic      <- select_k_bic
+ *   es_run_pipeline          <- run_pipeline
  *
  * Conventions
  *  - Plain pointers and sizes only.  Parameters are host FP64 arrays, row-major:
@@ -178,6 +179,31 @@ int es_gmm_calibrate(es_ctx* ctx, es_dataset* ds, const es_gmm_params* p, int64_
 /* bic[j] = NaN for a K that failed. */
 int es_gmm_select_k_bic(es_ctx* ctx, es_dataset* ds, const int32_t* k_range, int32_t n_k, const es_fit_opts* opts,
                         int32_t* best_k, double* bic);
+
+/* ---------------------------------------------------------- pipeline ---- */
+/* run_pipeline over a time-ordered feature matrix (row order = event
+ * order): the first floor(train_window * N) rows are the training split; columns are
+ * z-scored with the training split's mean and population standard deviation (a zero-
+ * variance column is centred only); a K-component GMM is fitted on the
+ * standardized training split; delta is the quantile_q-quantile of the training split's
+ * best-component densities, or cfg->delta when quantile_q <= 0; every
+ * row is then scored per detect.  InsufficientTraining if the training
+ * split has fewer than 10*K rows.  The model is in standardized space. */
+typedef struct {
+    int32_t K;
+    double train_window;   /* fraction of the earliest events used for fitting, SPEC.md:347 (0.5) */
+    double quantile_q;     /* > 0: calibrate delta (SPEC.md:394 default 0.01); <= 0: use delta */
+    double delta;          /* density threshold when quantile_q <= 0 */
+    int32_t standardize;   /* 1: z-score with training-split statistics */
+    int32_t mode;          /* 0: best-component density (Def. 1), 1: mixture density */
+    es_fit_opts fit;
+} es_pipeline_cfg;
+int es_run_pipeline(es_ctx* ctx, es_dataset* ds, const es_pipeline_cfg* cfg, es_gmm_params* model /* out */,
+                    es_fit_report* rep, double* std_mean /* D, nullable */, double* std_scale /* D, nullable */,
+                    double* delta, double* log_delta, uint8_t* flags /* n_local, nullable */,
+                    int32_t* best_k /* n_local, nullable */, double* best_logdens /* n_local, nullable */,
+                    int64_t* anomaly_indices /* n_local capacity, nullable */, int64_t* n_local_flagged,
+                    int64_t* n_flagged);
 
 #ifdef __cplusplus
 }

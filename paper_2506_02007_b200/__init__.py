@@ -59,6 +59,11 @@ class _FitOpts(C.Structure):
                 ("seed", C.c_uint64), ("covariance_type", C.c_int32)]
 
 
+class _PipelineCfg(C.Structure):
+    _fields_ = [("K", C.c_int32), ("train_window", C.c_double), ("quantile_q", C.c_double), ("delta", C.c_double),
+                ("standardize", C.c_int32), ("mode", C.c_int32), ("fit", _FitOpts)]
+
+
 class _FitReport(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("final_log_likelihood", C.c_double), ("converged", C.c_int32),
                 ("seed", C.c_uint64), ("n_per_iter", C.c_int32), ("collapses", C.c_int32),
@@ -487,3 +492,47 @@ def select_k_bic(X, k_range: Sequence[int], init="kmeans++", tol=1e-6, max_iter=
                                            C.c_int32(len(kr)), C.byref(o), C.byref(best),
                                            C.c_void_p(bic.ctypes.data)))
     return best.value, bic
+
+
+@dataclass
+class PipelineResult:
+    """run_pipeline: the model (standardized space), the standardization
+    (per-column mean, scale; scale 1 for a zero-variance column), the threshold and the
+    DetectionReport over ALL events."""
+    model: GmmModel
+    report: DetectionReport
+    mean: np.ndarray
+    scale: np.ndarray
+    n_train: int
+
+
+def run_pipeline(X, K: int, train_window: float = 0.5, quantile_q: Optional[float] = 0.01,
+                 delta: Optional[float] = None, standardize: bool = True, mode: str = "component",
+                 init="kmeans++", tol: float = 1e-6, max_iter: int = 200, reg: Optional[float] = None, seed: int = 0,
+                 ctx: Optional[Context] = None) -> PipelineResult:
+    """run_pipeline over a time-ordered feature matrix: fit on the standardized
+    first train_window fraction, calibrate delta as the quantile_q-quantile there (or use delta),
+    detect over every event.  Runs on the device end to end (es_run_pipeline)."""
+    ds = _as_dataset(X, ctx)
+    D, n = ds.D, ds.n_local
+    q = float(quantile_q) if quantile_q is not None and delta is None else 0.0
+    cfg = _PipelineCfg(int(K), float(train_window), q, float(delta) if delta is not None else 0.0,
+                       1 if standardize else 0, {"component": 0, "mixture": 1}[mode],
+                       _opts(init, tol, max_iter, reg, seed))
+    w, mu, cov = np.empty(K), np.empty((K, D)), np.empty((K, D, D))
+    p = _Params(K, D, w.ctypes.data, mu.ctypes.data, cov.ctypes.data)
+    rep = _FitReport()
+    mean, scale = np.empty(D), np.empty(D)
+    d, ld = C.c_double(), C.c_double()
+    fl, bk, bl = np.empty(n, np.uint8), np.empty(n, np.int32), np.empty(n)
+    idx = np.empty(max(n, 1), np.int64)
+    nloc, ng = C.c_int64(), C.c_int64()
+    _check(ds.ctx._lib.es_run_pipeline(ds.ctx.handle, ds.handle, C.byref(cfg), C.byref(p), C.byref(rep),
+                                       mean.ctypes.data_as(C.c_void_p), scale.ctypes.data_as(C.c_void_p),
+                                       C.byref(d), C.byref(ld), C.c_void_p(_ptr(fl)), C.c_void_p(_ptr(bk)),
+                                       C.c_void_p(_ptr(bl)), C.c_void_p(_ptr(idx)), C.byref(nloc), C.byref(ng)))
+    fr = FitReport(rep.iterations, rep.final_log_likelihood, np.zeros(0), bool(rep.converged), rep.seed,
+                   rep.collapses, rep.reg_used)
+    model = GmmModel(w, mu, cov, fr)
+    report = DetectionReport(fl, idx[:nloc.value].copy(), bk, bl, model, d.value, ld.value, ng.value)
+    return PipelineResult(model, report, mean, scale, int(np.floor(train_window * ds.n_global)))

@@ -920,6 +920,25 @@ __global__ void __launch_bounds__(256) k_unit_gram(const double* __restrict__ X,
     }
 }
 
+// Z[j][i] = (X[j][i] - mean[j]) * inv_scale[j], planar FP64 (run_pipeline standardization)
+__global__ void k_standardize(const double* __restrict__ X, int64_t n, int64_t ld, int D,
+                              const double* __restrict__ mean, const double* __restrict__ inv_scale,
+                              double* __restrict__ Z, int64_t zld) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int j = blockIdx.y; j < D; j += gridDim.y) {
+        const double m = mean[j], s = inv_scale[j];
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+            Z[(int64_t)j * zld + i] = (X[(int64_t)j * ld + i] - m) * s;
+    }
+}
+
+void launch_standardize(const double* X, int64_t n, int64_t ld, int D, const double* mean, const double* inv_scale,
+                        double* Z, int64_t zld, int num_sms, cudaStream_t s, LaunchStats& ls) {
+    if (n <= 0) return;
+    k_standardize<<<dim3(num_sms * 4, D), 256, 0, s>>>(X, n, ld, D, mean, inv_scale, Z, zld);
+    ++ls.launches;
+}
+
 void launch_unit_stats(const double* X, int64_t n, int64_t ld, int D, const double* center, double* partial,
                        int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls) {
     if (D <= 16) {

@@ -42,6 +42,9 @@ void launch_em_pass(const double* X, int64_t n, int64_t ld, int D, int K, const 
 // Unit-weight statistics about `center` (K = 1): data covariance pass.
 void launch_unit_stats(const double* X, int64_t n, int64_t ld, int D, const double* center, double* partial,
                        int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
+// Z = (X - mean) * inv_scale per feature plane (run_pipeline standardization).
+void launch_standardize(const double* X, int64_t n, int64_t ld, int D, const double* mean, const double* inv_scale,
+                        double* Z, int64_t zld, int num_sms, cudaStream_t s, LaunchStats& ls);
 // Fixed-order sum of nblk partial blocks of length len -> out.
 void launch_reduce_blocks(const double* partial, int nblk, int len, double* out, cudaStream_t s, LaunchStats& ls);
 // Column sum/min/max/non-finite count: out[4*D] = sum | min | max | nonfinite.

@@ -40,6 +40,8 @@ struct Fail {
 };
 
 [[noreturn]] void fail(int code, const std::string& name, const std::string& msg) { throw Fail{code, name, msg}; }
+// re-raise the error a nested es_* call just recorded
+[[noreturn]] void rethrow_last(int code) { throw Fail{code, g_name, g_msg}; }
 
 void cu_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) {
@@ -1043,6 +1045,98 @@ int es_dataset_generate(es_ctx* c, uint64_t seed, int64_t n_global, int32_t D, i
         finish_dataset(c, ds.get());
         *out = ds.release();
     });
+}
+
+// ---------------------------------------------------------------- pipeline
+// A dataset sharing `base`'s (or its own) planes, restricted to the global rows [0, n_rows)
+// (`own` = false: the view never frees X).
+static es_dataset* make_view(es_ctx* c, es_dataset* base, double* X, int64_t n_rows) {
+    auto v = std::make_unique<es_dataset>();
+    v->ctx = c;
+    v->D = base->D;
+    v->ld = base->ld;
+    v->X = X;
+    v->n_local = std::max<int64_t>(0, std::min(base->n_local, n_rows - base->row_offset));
+    finish_dataset(c, v.get());
+    return v.release();
+}
+
+int es_run_pipeline(es_ctx* c, es_dataset* ds, const es_pipeline_cfg* cfg, es_gmm_params* model, es_fit_report* rep,
+                    double* std_mean, double* std_scale, double* delta, double* log_delta, uint8_t* flags,
+                    int32_t* best_k, double* best_logdens, int64_t* anomaly_indices, int64_t* n_local_flagged,
+                    int64_t* n_flagged) {
+    struct Views {  // views do not own their planes; the standardized copy is owned here
+        es_dataset* train = nullptr;
+        es_dataset* all = nullptr;
+        es_dataset* ztrain = nullptr;
+        double* Z = nullptr;
+        ~Views() {
+            for (es_dataset* v : {train, ztrain}) {
+                if (v) v->X = nullptr;
+                delete v;
+            }
+            if (all) all->X = nullptr;
+            delete all;
+            if (Z) cudaFree(Z);
+        }
+    } V;
+    int status = guard([&] {
+        CU(cudaSetDevice(c->device));
+        if (!cfg || !model || !delta || !log_delta) fail(ES_ERR_DATA, "InvalidArgument", "null argument");
+        const int D = ds->D, K = cfg->K;
+        if (model->K != K || model->D != D) fail(ES_ERR_DATA, "DimensionMismatch", "model buffers do not match K, D");
+        if (!(cfg->train_window > 0.0 && cfg->train_window <= 1.0))
+            fail(ES_ERR_DATA, "RangeViolation", "train_window must be in (0,1]");
+        if (ds->n_global < 1) fail(ES_ERR_DATA, "EmptyLayer", "no events");
+        const int64_t n_train = (int64_t)std::floor(cfg->train_window * (double)ds->n_global);
+        if (n_train < 10 * (int64_t)K)
+            fail(ES_ERR_DATA, "InsufficientTraining", "training split has fewer than 10*K events");
+        if (!(cfg->quantile_q > 0.0) && !(cfg->delta > 0.0))
+            fail(ES_ERR_DATA, "RangeViolation", "need quantile_q in (0,1) or delta > 0");
+        // training-split statistics (rank-ordered sums: identical on every rank)
+        std::vector<double> mean(D, 0.0), scale(D, 1.0);
+        V.train = make_view(c, ds, ds->X, n_train);
+        if (cfg->standardize) {
+            const DataStats st = data_stats(c, V.train);
+            if (st.nonfinite > 0) fail(ES_ERR_DATA, "NonFiniteFeature", "X contains non-finite entries");
+            for (int j = 0; j < D; ++j) {
+                mean[j] = st.mean[j];
+                const double var = st.S[(size_t)j * D + j];
+                scale[j] = var > 0.0 ? std::sqrt(var) : 1.0;  // zero variance: centred only
+            }
+            // standardized copy of every local row
+            CU(cudaMalloc(&V.Z, (size_t)ds->ld * D * 8));
+            std::vector<double> ms(2 * D);
+            for (int j = 0; j < D; ++j) {
+                ms[j] = mean[j];
+                ms[D + j] = 1.0 / scale[j];
+            }
+            double* dms = c->scratch2.as<double>(2 * D);
+            CU(cudaMemcpyAsync(dms, ms.data(), 2 * D * 8, cudaMemcpyHostToDevice, c->stream));
+            launch_standardize(ds->X, ds->n_local, ds->ld, D, dms, dms + D, V.Z, ds->ld, c->num_sms, c->stream,
+                               c->ls);
+            c->check_launch();
+            V.all = make_view(c, ds, V.Z, ds->n_global);
+            V.ztrain = make_view(c, ds, V.Z, n_train);
+        }
+        es_dataset* fit_ds = cfg->standardize ? V.ztrain : V.train;
+        es_dataset* all_ds = cfg->standardize ? V.all : ds;
+        es_fit_report r{};
+        if (int e = es_gmm_fit(c, fit_ds, K, &cfg->fit, nullptr, model, rep ? rep : &r, nullptr)) rethrow_last(e);
+        if (cfg->quantile_q > 0.0) {
+            if (int e = es_gmm_calibrate(c, all_ds, model, n_train, cfg->quantile_q, cfg->mode, delta, log_delta))
+                rethrow_last(e);
+        } else {
+            *delta = cfg->delta;
+            *log_delta = std::log(cfg->delta);
+        }
+        if (int e = es_gmm_detect(c, all_ds, model, *log_delta, cfg->mode, flags, best_k, best_logdens,
+                                  anomaly_indices, n_local_flagged, n_flagged))
+            rethrow_last(e);
+        if (std_mean) std::copy(mean.begin(), mean.end(), std_mean);
+        if (std_scale) std::copy(scale.begin(), scale.end(), std_scale);
+    });
+    return status;
 }
 
 int es_dataset_destroy(es_dataset* ds) {

@@ -230,6 +230,46 @@ double calibrate_threshold(const GmmModel& model, const FeatureMatrix& X_train, 
     return calibrate_threshold_log(model, X_train, q, mode).first;
 }
 
+PipelineResult run_pipeline(const FeatureMatrix& X, const DetectorConfig& cfg, const FitOptions& opts,
+                            bool standardize) {
+    Dataset ds;
+    upload(X, ds);
+    const int d = X.dim, K = cfg.K;
+    es_pipeline_cfg c{};
+    c.K = K;
+    c.train_window = cfg.train_window;
+    c.quantile_q = cfg.delta ? 0.0 : cfg.quantile_q.value_or(0.0);
+    c.delta = cfg.delta.value_or(0.0);
+    c.standardize = standardize ? 1 : 0;
+    c.mode = cfg.mode == DetectMode::Mixture ? ES_DETECT_MIXTURE : ES_DETECT_COMPONENT;
+    c.fit = c_opts(opts);
+    PipelineResult r;
+    GmmModel& m = r.report.model;
+    m.K = K;
+    m.d = d;
+    m.weights.resize(std::max(K, 0));
+    m.means.resize((size_t)std::max(K, 0) * d);
+    m.covariances.resize((size_t)std::max(K, 0) * d * d);
+    es_gmm_params out{K, d, m.weights.data(), m.means.data(), m.covariances.data()};
+    es_fit_report rep{};
+    std::vector<double> mean(d), scale(d);
+    std::vector<int32_t> bk(X.rows);
+    std::vector<int64_t> idx(std::max<int64_t>(X.rows, 1));
+    r.report.flags.resize(X.rows);
+    r.report.log_density.resize(X.rows);
+    int64_t nloc = 0, ng = 0;
+    check(es_run_pipeline(ctx(), ds.ds, &c, &out, &rep, mean.data(), scale.data(), &r.report.delta,
+                          &r.report.log_delta, r.report.flags.data(), bk.data(), r.report.log_density.data(),
+                          idx.data(), &nloc, &ng));
+    m.fit_report = FitReport{rep.iterations, rep.final_log_likelihood, {}, rep.converged != 0, rep.seed};
+    idx.resize(nloc);
+    r.report.anomaly_indices = std::move(idx);
+    r.report.best_component.assign(bk.begin(), bk.end());
+    for (int j = 0; j < d; ++j) r.standardization.emplace_back(mean[j], scale[j]);
+    r.n_train = (std::int64_t)std::floor(cfg.train_window * (double)X.rows);
+    return r;
+}
+
 // ------------------------------------------------------------------ JSON
 namespace {
 

@@ -37,6 +37,14 @@ int main() {
     const double delta = calibrate_threshold(m, X, 0.01);
     DetectionReport r2 = detect(m, X, delta);
     ok = ok && r2.anomaly_indices.size() <= 20;
+    // run_pipeline: standardize on the train window, fit, calibrate on it, detect all rows
+    FeatureMatrix Xi;  // interleave the two clusters so the train window holds both
+    Xi.rows = X.rows;
+    Xi.dim = 1;
+    for (int i = 0; i < 1000; ++i) Xi.data.insert(Xi.data.end(), {X.data[i], X.data[1000 + i]});
+    PipelineResult pr = run_pipeline(Xi, DetectorConfig{std::nullopt, 0.01, 2, 0.5, DetectMode::Component}, FitOptions{});
+    ok = ok && pr.report.flags.size() == (size_t)X.rows && pr.standardization.size() == (size_t)X.dim &&
+         pr.n_train == X.rows / 2 && pr.report.delta > 0.0 && pr.report.model.K == 2;
     // JSON round trip (within 1e-15 per entry)
     GmmModel back = model_from_json(to_json(m));
     for (size_t i = 0; i < m.covariances.size(); ++i) ok = ok && back.covariances[i] == m.covariances[i];

@@ -286,3 +286,45 @@ def test_small_components_use_strict_passes(es, oracle):
     assert_params(m, pi, mu, cov)
     assert np.all(np.abs(m.fit_report.per_iteration_log_likelihoods - rep["per_iteration_log_likelihoods"])
                   <= LL_TOL * np.abs(rep["per_iteration_log_likelihoods"]))
+
+
+# ------------------------------------------------ run_pipeline
+def test_run_pipeline_parity(es, oracle):
+    """run_pipeline on the device vs the oracle composition: train split =
+    first half of the (time-ordered) rows, z-scored with its mean and population std; fit;
+    q-quantile threshold on the train split; detect over all rows."""
+    n, D, K = 200_000, 8, 4
+    ds, X = syn(es, oracle, n, D, K, seed=11)
+    r = es.run_pipeline(ds, K, train_window=0.5, quantile_q=0.01, init="random", tol=0.0, max_iter=25, seed=3)
+    n_train = n // 2
+    m, s = X[:n_train].mean(0), X[:n_train].std(0)
+    assert r.n_train == n_train
+    assert np.allclose(r.mean, m, rtol=1e-12, atol=1e-12) and np.allclose(r.scale, s, rtol=1e-12)
+    Z = (X - m) / s
+    pi, mu, cov, rep = oracle.fit_em(Z[:n_train], K, init="random", tol=0.0, max_iter=25, seed=3)
+    assert_params(r.model, pi, mu, cov)
+    # threshold and flags on the pipeline's own model (identical model on both sides)
+    od, old = oracle.calibrate(Z[:n_train], r.model.weights, r.model.means, r.model.covariances, 0.01)
+    assert abs(r.report.log_delta - old) <= 1e-9 * max(1.0, abs(old))
+    of, obk, obl, on = oracle.detect(Z, r.model.weights, r.model.means, r.model.covariances, r.report.log_delta)
+    mism = np.nonzero(r.report.flags != of)[0]
+    assert np.all(np.abs(obl[mism] - r.report.log_delta) < BAND)
+    assert np.array_equal(r.report.anomaly_indices, np.nonzero(r.report.flags)[0])
+    assert_ll(r.report.log_density, obl)
+    # the calibration guarantee on the training split (SPEC.md:370)
+    assert r.report.flags[:n_train].sum() <= math.ceil(0.01 * n_train)
+
+
+def test_run_pipeline_errors_and_fixed_delta(es, oracle):
+    ds, X = syn(es, oracle, 60, 2, 2, seed=5)
+    with pytest.raises(es.EventscopeError) as e:
+        es.run_pipeline(ds, 4, train_window=0.5)  # 30 training rows < 10 K
+    assert e.value.name == "InsufficientTraining" and e.value.kind == "Data"
+    # fixed delta, no standardization: detect runs on the raw features with that delta
+    ds2, X2 = syn(es, oracle, 50_000, 3, 2, seed=6)
+    r = es.run_pipeline(ds2, 2, train_window=0.4, quantile_q=None, delta=1e-3, standardize=False, init="random",
+                        tol=0.0, max_iter=10, seed=1)
+    assert np.all(r.mean == 0) and np.all(r.scale == 1) and abs(r.report.delta - 1e-3) < 1e-18
+    of, _, obl, _ = oracle.detect(X2, r.model.weights, r.model.means, r.model.covariances, np.log(1e-3))
+    mism = np.nonzero(r.report.flags != of)[0]
+    assert np.all(np.abs(obl[mism] - np.log(1e-3)) < BAND)
