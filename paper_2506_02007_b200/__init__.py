@@ -85,10 +85,12 @@ def load_library() -> C.CDLL:
     """Load the in-tree CUDA library (fails loudly if it was not built)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(_LIB_PATH):
+        # ES_LIB_OVERRIDE: an instrumented in-tree build of the same library (scripts/em_trace.sh)
+        path = os.environ.get("ES_LIB_OVERRIDE") or _LIB_PATH
+        if not os.path.exists(path):
             raise EventscopeError("Io", "NotBuilt",
-                                  f"{_LIB_PATH} missing; run __graft_entry__.build() (no CPU fallback exists)")
-        lib = C.CDLL(_LIB_PATH)
+                                  f"{path} missing; run __graft_entry__.build() (no CPU fallback exists)")
+        lib = C.CDLL(path)
         lib.es_last_error_name.restype = C.c_char_p
         lib.es_last_error_message.restype = C.c_char_p
         lib.es_version.restype = C.c_char_p

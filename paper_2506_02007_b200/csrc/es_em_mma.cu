@@ -42,51 +42,75 @@
 #include "es_kernels.h"
 #include "es_mma.cuh"
 
+#ifndef ES_EM_KB
+#define ES_EM_KB 2
+#endif
+
 namespace es {
+
+#ifdef ES_EM_TRACE
+// debug timeline of CTA 0 (scripts/em_trace.py): clock64 per (event, tile)
+constexpr int TR_EV = 12, TR_T = 128;
+__device__ long long g_em_trace[TR_EV][TR_T];
+#define TRACE(ev, j)                                                          \
+    do {                                                                      \
+        if (blockIdx.x == 0 && (j) < TR_T) g_em_trace[ev][(j)] = clock64();   \
+    } while (0)
+#else
+#define TRACE(ev, j) \
+    do {             \
+    } while (0)
+#endif
 
 namespace {
 
 using namespace mma;
 
-constexpr int NTHR = 320;              // WG0, WG1 (alternate tiles), warp 8 TMA, warp 9 MMA
+// NWG epilogue warpgroups take tiles round robin (2; 3 is an NPASS = 1 option,
+// ES_EM_MMA_WG), then a TMA warp and an MMA-issuer warp.
+constexpr int nthr(int nwg) { return 128 * nwg + 64; }
 constexpr uint32_t GRP = (TM / 8) * 128;   // one MN-major group of 8 columns: 16 K-groups x 128 B
-constexpr uint32_t RECH = 19 * GRP;        // 38912 B
 constexpr uint32_t RECL = 16 * GRP;        // 32768 B
-constexpr int MREG0 = 128, MREGS = 144;    // Gram regions at TMEM columns [128, 272) and [272, 416)
-constexpr int TA0 = 416;                   // x^ hi/lo E-step A operands: WG w at [416 + 16 w, +16)
-constexpr int TONE = 448;                  // ones in K columns 0, 1 (bias dispatch A operand)
+constexpr int MREG0 = 128;                 // two Gram regions (tile parity) from TMEM column 128
+constexpr int mregs(int npass) { return npass == 2 ? 144 : 136; }
+constexpr int ta0(int npass) { return MREG0 + 2 * mregs(npass); }  // x^ hi/lo A operands, 16 columns per WG
+constexpr int tone(int npass, int nwg) { return ta0(npass) + 16 * nwg; }  // ones (bias dispatch A operand)
+static_assert(tone(1, 3) + 8 <= 512 && tone(2, 2) + 8 <= 512, "TMEM columns");
 
-template <int NPASS>
+template <int NPASS, int NWG>
 struct Smem {
     static constexpr int XS = NPASS == 2 ? 3 : 4;       // FP64 tile stages (TMA)
+    static constexpr uint32_t RECH = (NPASS == 2 ? 19 : 17) * GRP;
     double xd[XS][DM * TM];                             // 48 / 64 KB  FP64 tiles (planar, TMA destination)
-    unsigned char rech[2][RECH];                        // 76 KB  hi records (per warpgroup)
-    unsigned char recl[2][NPASS == 2 ? RECL : 16];      // 64 KB  2 x lo records
+    unsigned char rech[NWG][RECH];                      // hi records (per warpgroup)
+    unsigned char recl[NPASS == 2 ? NWG : 1][NPASS == 2 ? RECL : 16];  // 2 x lo records
     unsigned char bw[2][OPB];                           // W' hi / lo
     unsigned char bb[OPB];                              // b' hi, lo in K columns 0, 1
     double c[DM];
-    double shift[2][KMAX * DM];                         // record centre - starting centre (FP64, exact)
-    double dl[2][KMAX * DM], s1x[2][KMAX * DM];         // recentring exchange
-    double wred[8][KMAX + 1];                           // per-warp partial N_k | logL
-    double ntot[2][KMAX];
-    float nmu[2][KMAX * DM];                            // -(record centre), x^ units, FP32
+    double shift[NWG][KMAX * DM];                       // record centre - starting centre (FP64, exact)
+    double dl[NWG][KMAX * DM], s1x[NWG][KMAX * DM];     // recentring exchange
+    double wred[4 * NWG][KMAX + 1];                     // per-warp partial N_k | logL
+    double ntot[NWG][KMAX];
+    float nmu[NWG][KMAX * DM];                          // -(record centre), x^ units, FP32
     float cst[KMAX];                                    // log pi_k + lognorm_k
     float hq[KMAX];                                     // 0.5 t_k^2
     float tk[KMAX];
-    uint64_t xfull[XS], xfree[XS], aeready[2], edone[2], mready[2], mdone[2], efree;
+    uint64_t xfull[XS], xfree[XS], aeready[NWG], edone[NWG], mready[NWG], mdone[NWG], rfree[2], efree;
     uint32_t tmem;
 };
 
 }  // namespace
 
-template <int NPASS, bool F32>
-__global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUtensorMap xmap, int64_t n, int D,
-                                                     int K, const double* __restrict__ model,
-                                                     const double* __restrict__ center, double xs,
-                                                     const __grid_constant__ NegCx ncx, const float2 xsf_c,
-                                                     double* __restrict__ partial) {
-    using Sm = Smem<NPASS>;
-    constexpr int XS = Sm::XS;
+template <int NPASS, bool F32, int NWG>
+__global__ void __launch_bounds__(nthr(NWG), 1) k_em_mma(const __grid_constant__ CUtensorMap xmap, int64_t n, int D,
+                                                          int K, const double* __restrict__ model,
+                                                          const double* __restrict__ center, double xs,
+                                                          const __grid_constant__ NegCx ncx,
+                                                          const __grid_constant__ NegCxF ncxf, const float xsf,
+                                                          int policy, double* __restrict__ partial) {
+    using Sm = Smem<NPASS, NWG>;
+    constexpr int XS = Sm::XS, NTHR = nthr(NWG), MREGS = mregs(NPASS), TA0 = ta0(NPASS), TONE = tone(NPASS, NWG);
+    constexpr int WTMA = 4 * NWG, WMMA = 4 * NWG + 1;
     extern __shared__ __align__(128) unsigned char smraw[];
     // keep the shared-window provenance of the pointer (generic LD/ST otherwise)
     Sm& S = *reinterpret_cast<Sm*>(smraw + ((128u - (su32(smraw) & 127u)) & 127u));
@@ -102,10 +126,12 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
     for (int e = t; e < KMAX * DM; e += NTHR) {
         const int k = e / DM, f = e % DM;
         const float m0 = (k < K && f < D) ? -(float)((mv.mu()[k * D + f] - center[f]) * xs) : 0.f;
-        S.nmu[0][e] = S.nmu[1][e] = m0;
-        S.shift[0][e] = S.shift[1][e] = 0.0;
+        for (int w = 0; w < NWG; ++w) {
+            S.nmu[w][e] = m0;
+            S.shift[w][e] = 0.0;
+        }
     }
-    if (warp == 9) {
+    if (warp == WMMA) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&S.tmem)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
@@ -114,12 +140,13 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
             mbar_init(&S.xfull[i], 1);
             mbar_init(&S.xfree[i], 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < NWG; ++i) {
             mbar_init(&S.aeready[i], 1);
             mbar_init(&S.edone[i], 1);
             mbar_init(&S.mready[i], 4);
             mbar_init(&S.mdone[i], 1);
         }
+        for (int i = 0; i < 2; ++i) mbar_init(&S.rfree[i], 4);
         mbar_init(&S.efree, 4);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -138,22 +165,25 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
     __syncthreads();
     tc_fence_after();
 
-    if (warp < 8) {
+    if (warp < WTMA) {
         // ====================================================== epilogue warpgroups
-        // WG w takes tiles j = w, w + 2, ...: converts its FP64 tile, then (thread =
+        // WG w takes tiles j = w, w + NWG, ...: converts its FP64 tile, then (thread =
         // event = TMEM lane) reads U, forms the responsibilities and the records; as
-        // thread = (k, a) it flushes its own Gram region.
+        // thread = (k, a) it flushes the Gram of its tile (region j & 1) and releases it.
         const int w = warp >> 2;
         const int p = t & 127;             // event row of the tile / Gram row (k, a)
         const int q = warp & 3;            // TMEM lane quadrant
         const uint32_t lq = (uint32_t)(32 * q) << 16;
         const int hsel = lane >> 4;        // Gram row (k, a): k = 2q + hsel, a = lane & 15
         const int kk = p >> 4, aa = p & 15;
+        // three warpgroups (128 registers): constants from shared memory, next tile
+        // converted after the records instead of being held in registers across them
+        constexpr bool LATE = NWG == 3;
         float cst[KMAX], hq[KMAX];
 #pragma unroll
         for (int k = 0; k < KMAX; ++k) {
-            cst[k] = S.cst[k];
-            hq[k] = S.hq[k];
+            cst[k] = LATE ? 0.f : S.cst[k];
+            hq[k] = LATE ? 0.f : S.hq[k];
         }
         // statistics in compensated FP32 pairs (hi, lo): Gram row, first moment, N_k; logL in FP64
         uint64_t g2h[DM / 2], g2l[DM / 2], nkh[KMAX / 2], nkl[KMAX / 2];
@@ -169,10 +199,12 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
             lo = pack2((float)(a - (double)ah), (float)(b - (double)bh));
         };
 
-        auto flush = [&](int64_t jj) {  // Gram of this WG's local tile jj -> FP64
+        auto flush = [&](int64_t jj) {  // Gram of this WG's local tile jj (tile w + NWG jj) -> FP64
+            if (p == 0) TRACE(6, w + NWG * jj);
             mbar_wait(su32(&S.mdone[w]), (uint32_t)(jj & 1));
             tc_fence_after();
-            const uint32_t xg = (uint32_t)(MREG0 + MREGS * w);
+            const int rg = (int)((w + NWG * jj) & 1);
+            const uint32_t xg = (uint32_t)(MREG0 + MREGS * rg);
             float v[32], f0, f1, m1;
             tmem_ld32(tmem + lq + xg + 32 * q, v);
             tmem_ld2(tmem + lq + xg + TM + 2 * q, f0, f1);
@@ -190,6 +222,9 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
                 cacc2(g2h[b / 2], g2l[b / 2], hsel ? pack2(v[16 + b], v[17 + b]) : pack2(v[b], v[b + 1]));
             cacc(g1h, g1l, m1);
             tc_fence_before();
+            __syncwarp();
+            if (lane == 0) arrive(&S.rfree[rg]);
+            if (p == 0) TRACE(7, w + NWG * jj);
         };
         // N_k of this WG (fixed-order reduction) -> S.ntot[w]
         auto wg_counts = [&]() {
@@ -198,13 +233,13 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
                 const double v = warp_sum(cval(nkh[k >> 1], nkl[k >> 1], k & 1));
                 if (lane == 0) S.wred[warp][k] = v;
             }
-            named_sync(3 + w, 128);
+            named_sync(4 + w, 128);
             if (p < KMAX) {
                 double s = 0.0;
                 for (int i = 0; i < 4; ++i) s += S.wred[4 * w + i][p];
                 S.ntot[w][p] = s;
             }
-            named_sync(3 + w, 128);
+            named_sync(4 + w, 128);
         };
         // Move this WG's accumulation centre for component k to its running estimate of
         // the new mean (x^ units, rounded to FP32 for the records) and re-express the
@@ -225,7 +260,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
             }
             S.dl[w][p] = d;
             S.s1x[w][p] = g1;
-            named_sync(3 + w, 128);
+            named_sync(4 + w, 128);
 #pragma unroll
             for (int bb = 0; bb < DM; bb += 2) {
                 double nv[2];
@@ -243,7 +278,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
                 S.nmu[w][p] = -(float)(-(double)S.nmu[w][p] + d);
                 S.shift[w][p] += d;
             }
-            named_sync(3 + w, 128);
+            named_sync(4 + w, 128);
         };
 
         bool pend = false;   // the Gram of this WG's previous tile is still to be flushed
@@ -258,8 +293,8 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
             for (int f = 0; f < DM; f += 2) {
                 float v0, v1;
                 if (F32) {  // FP32 pipe: x within 4x of its spread about c (see launch_em_mma)
-                    v0 = fmaf(__double2float_rn(S.xd[s][f * TM + p]), xsf_c.x, (float)ncx.v[f]);
-                    v1 = fmaf(__double2float_rn(S.xd[s][(f + 1) * TM + p]), xsf_c.x, (float)ncx.v[f + 1]);
+                    v0 = fmaf(__double2float_rn(S.xd[s][f * TM + p]), xsf, ncxf.v[f]);
+                    v1 = fmaf(__double2float_rn(S.xd[s][(f + 1) * TM + p]), xsf, ncxf.v[f + 1]);
                 } else {
                     v0 = (float)fma(S.xd[s][f * TM + p], xs, ncx.v[f]);
                     v1 = (float)fma(S.xd[s][(f + 1) * TM + p], xs, ncx.v[f + 1]);
@@ -268,7 +303,9 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
                 const uint32_t h = pack_h2(v0, v1);
                 const float2 hf = __half22float2(u2h(h));
                 hw[f / 2] = h;
-                lw[f / 2] = pack_h2(v0 - hf.x, v1 - hf.y);
+                float l0, l1;
+                unpack2(sub2(x2[f / 2], pack2(hf.x, hf.y)), l0, l1);
+                lw[f / 2] = pack_h2(l0, l1);
             }
             tmem_st8(tmem + lq + TA0 + 16 * w, hw);
             tmem_st8(tmem + lq + TA0 + 16 * w + 8, lw);
@@ -278,39 +315,55 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
             if (p == 0) {
                 arrive(&S.xfree[s]);
                 arrive(&S.aeready[w]);
+                TRACE(5, j);
             }
         };
         uint64_t x2[DM / 2], x2n[DM / 2];
         if (w < J) convert(w, x2);
-        for (int64_t j = w; j < J; j += 2, ++jj) {
+        for (int64_t j = w; j < J; j += NWG, ++jj) {
             const bool valid = tile_of(j) * TM + p < n;
             // ---- E-step epilogue
             mbar_wait(su32(&S.edone[w]), (uint32_t)(jj & 1));
             tc_fence_after();
+            if (p == 0) TRACE(3, j);
             float wk[KMAX];
             float mx = -INFINITY;
+            // U in batches of KB components (one TMEM load wait per batch); the E region is
+            // released as soon as the last batch is in registers
+            constexpr int KB = ES_EM_KB;
 #pragma unroll
-            for (int k = 0; k < KMAX; ++k) {
-                float u[16];
-                tmem_ld16(tmem + lq + 16 * k, u);
+            for (int k0 = 0; k0 < KMAX; k0 += KB) {
+                float u[KB][16];
+#pragma unroll
+                for (int k = 0; k < KB; ++k) tmem_ld16(tmem + lq + 16 * (k0 + k), u[k]);
                 tmem_wait_ld();
-                uint64_t q2 = 0;
-#pragma unroll
-                for (int r = 0; r < 16; r += 2) {
-                    const uint64_t uu = pack2(u[r], u[r + 1]);
-                    ffma2(q2, uu, uu);
+                if (k0 + KB == KMAX) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) arrive(&S.efree);
+                    if (p == 0) TRACE(4, j);
                 }
-                float qa, qb;
-                unpack2(q2, qa, qb);
-                wk[k] = cst[k] - hq[k] * (qa + qb);
-                mx = fmaxf(mx, wk[k]);
+#pragma unroll
+                for (int k = 0; k < KB; ++k) {
+                    uint64_t q2 = 0, q3 = 0;
+#pragma unroll
+                    for (int r = 0; r < 16; r += 4) {
+                        const uint64_t ua = pack2(u[k][r], u[k][r + 1]), ub = pack2(u[k][r + 2], u[k][r + 3]);
+                        ffma2(q2, ua, ua);
+                        ffma2(q3, ub, ub);
+                    }
+                    float qa, qb, qc, qd;
+                    unpack2(q2, qa, qb);
+                    unpack2(q3, qc, qd);
+                    const int kk2 = k0 + k;
+                    wk[kk2] = LATE ? S.cst[kk2] - S.hq[kk2] * ((qa + qb) + (qc + qd))
+                                   : cst[kk2] - hq[kk2] * ((qa + qb) + (qc + qd));
+                    mx = fmaxf(mx, wk[kk2]);
+                }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) arrive(&S.efree);
             // E(j) has consumed this WG's A operand: stage the next tile now, so that its
             // E-step is ready long before this tile's records are
-            if (j + 2 < J) convert(j + 2, x2n);
+            if (!LATE && j + NWG < J) convert(j + NWG, x2n);
             float ssum = 0.f;
 #pragma unroll
             for (int k = 0; k < KMAX; ++k) ssum += ex2((wk[k] - mx) * 1.4426950408889634f);
@@ -332,7 +385,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
                 pend = false;
             }
             unsigned char* rh = S.rech[w] + (p >> 3) * 128 + (p & 7) * 16;
-            unsigned char* rl = S.recl[w] + (p >> 3) * 128 + (p & 7) * 16;
+            unsigned char* rl = S.recl[NPASS == 2 ? w : 0] + (p >> 3) * 128 + (p & 7) * 16;
 #pragma unroll
             for (int k = 0; k < KMAX; ++k) {
                 const uint64_t s2 = pack2(sg[k], sg[k]);
@@ -384,20 +437,25 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
             proxy_fence();
             __syncwarp();
             if (lane == 0) arrive(&S.mready[w]);
+            if (p == 0) TRACE(8, j);
             pend = true;
             // recentre after local tiles 1, 2, 4, 8, ... (drain this WG's Gram first)
-            if (((jj + 1) & jj) == 0 && j + 2 < J) {
+            if (((jj + 1) & jj) == 0 && j + NWG < J) {
                 flush(jj);
                 pend = false;
                 recentre(false);
             }
+            if (LATE) {
+                if (j + NWG < J) convert(j + NWG, x2);
+            } else {
 #pragma unroll
-            for (int r = 0; r < DM / 2; ++r) x2[r] = x2n[r];
+                for (int r = 0; r < DM / 2; ++r) x2[r] = x2n[r];
+            }
         }
         if (pend) flush(jj - 1);
         recentre(true);
         // -------------------------------------------------------------- output
-        // Sum the two WGs' statistics (fixed order) about the starting centre
+        // Sum the WGs' statistics (fixed order) about the starting centre
         // c + mu^_k / xs (x units; scale by xs^-1, xs^-2, exact) and symmetrise the
         // Gram, sym(P) = (P + P^T) / 2.  The record buffers are free now (scratch).
 #pragma unroll
@@ -409,87 +467,102 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
             const double v = warp_sum((double)llh + (double)lll);
             if (lane == 0) S.wred[warp][KMAX] = v;
         }
-        double* rows = reinterpret_cast<double*>(&S.rech[0][0]);  // [2][128][17]
-        named_sync(5, 256);  // both WGs drained: no Gram still reads the record buffers
+        double* rows = reinterpret_cast<double*>(&S.rech[0][0]);  // [NWG][128][17]
+        static_assert(sizeof(S.rech) >= NWG * TM * (DM + 1) * sizeof(double), "output scratch");
+        named_sync(7, 128 * NWG);  // all WGs drained: no Gram still reads the record buffers
 #pragma unroll
         for (int b = 0; b < DM; ++b) rows[(w * TM + p) * (DM + 1) + b] = g2v(b);
         rows[(w * TM + p) * (DM + 1) + DM] = (double)g1h + (double)g1l;
-        named_sync(5, 256);
+        named_sync(7, 128 * NWG);
         if (w == 0) {
             const int SK = stat_k(D), NE = K * SK;
             double* myp = partial + (int64_t)blockIdx.x * (NE + 1);
             const double i1 = 1.0 / xs, i2 = i1 * i1;
+            auto wsum = [&](int row, int col) {  // fixed WG order
+                double s = 0.0;
+#pragma unroll
+                for (int g = 0; g < NWG; ++g) s += rows[(g * TM + row) * (DM + 1) + col];
+                return s;
+            };
             if (kk < K && aa < D) {
                 double* blk = myp + kk * SK;
-                const double* r0 = rows + p * (DM + 1);
-                const double* r1 = rows + (TM + p) * (DM + 1);
-                blk[1 + aa] = (r0[DM] + r1[DM]) * i1;
-                for (int bb = aa; bb < D; ++bb) {
-                    const double* c0 = rows + (kk * DM + bb) * (DM + 1);
-                    const double* c1 = rows + (TM + kk * DM + bb) * (DM + 1);
-                    blk[1 + D + packed_index(aa, bb, D)] = 0.5 * ((r0[bb] + r1[bb]) + (c0[aa] + c1[aa])) * i2;
-                }
+                blk[1 + aa] = wsum(p, DM) * i1;
+                for (int bb = aa; bb < D; ++bb)
+                    blk[1 + D + packed_index(aa, bb, D)] = 0.5 * (wsum(p, bb) + wsum(kk * DM + bb, aa)) * i2;
             }
             if (p < K) {
                 double s = 0.0;
-                for (int i = 0; i < 8; ++i) s += S.wred[i][p];
+                for (int i = 0; i < 4 * NWG; ++i) s += S.wred[i][p];
                 myp[p * SK] = s;
             }
             if (p == KMAX) {
                 double s = 0.0;
-                for (int i = 0; i < 8; ++i) s += S.wred[i][KMAX];
+                for (int i = 0; i < 4 * NWG; ++i) s += S.wred[i][KMAX];
                 myp[NE] = s;
             }
         }
-    } else if (warp == 8) {
+    } else if (warp == WTMA) {
         // ========================================================== TMA producer
         if (lane == 0) {
             for (int64_t j = 0; j < J; ++j) {
                 const int s = (int)(j % XS);
                 if (j >= XS) mbar_wait_sleep(su32(&S.xfree[s]), (uint32_t)(((j - XS) / XS) & 1));
+                TRACE(0, j);
                 mbar_expect_tx(su32(&S.xfull[s]), (uint32_t)(D * TM * 8));
                 tma_load_2d(su32(&S.xd[s][0]), &xmap, (int)(tile_of(j) * TM), 0, su32(&S.xfull[s]));
             }
         }
-    } else {
+    } else if (warp == WMMA) {
         // ========================================================== MMA issuer
         if (lane == 0) {
-            const uint64_t dbh = sdesc(su32(S.bw[0]), 128, 256), dbl = sdesc(su32(S.bw[1]), 128, 256);
-            const uint64_t dbb = sdesc(su32(S.bb), 128, 256);
             constexpr uint32_t idesc1 = idesc_f16(128, NPASS == 2 ? 144 : 136, 1);
             constexpr uint32_t idesc2a = idesc_f16(128, 128, 1);
             constexpr uint32_t idesc2b = idesc_f16(128, 8, 1);
             // pass 1: D1 = R_h^T [R_h | s_h | s_l]; pass 2: P = D1 + (2 R_l)^T R_h on the Gram
             // columns, + (2 R_l)^T (s_h / 2) = R_l^T s_h on the s_h columns.
-            auto gram = [&](int64_t m) {
-                const int mw = (int)(m & 1);
-                tc_fence_after();
-                const uint32_t xg = tmem + (uint32_t)(MREG0 + MREGS * mw);
-                const uint32_t h0 = su32(S.rech[mw]), l0 = su32(S.recl[mw]);
+            // Gram of tile m (records of WG m % NWG into region m & 1).  Descriptors are
+            // precomputed per records buffer; a K-step adds 256 B (16 in the address field).
+            uint64_t dh0[NWG], dl0[NWG];
 #pragma unroll
-                for (int ks = 0; ks < TM / 16; ++ks) {
-                    const uint64_t dh = sdesc(h0 + ks * 256, 128, GRP);
-                    mma_f16(xg, dh, dh, idesc1, ks > 0 ? 1u : 0u);
-                }
+            for (int g = 0; g < NWG; ++g) {
+                dh0[g] = sdesc(su32(S.rech[g]), 128, GRP);
+                dl0[g] = sdesc(su32(S.recl[NPASS == 2 ? g : 0]), 128, GRP);
+            }
+            auto gram = [&](int64_t m) {
+                const int mw = (int)(m % NWG);
+                const uint32_t xg = tmem + (uint32_t)(MREG0 + MREGS * (int)(m & 1));
+                const uint64_t dh = mw == 0 ? dh0[0] : (mw == 1 ? dh0[1] : dh0[NWG - 1]);
+                const uint64_t dl = mw == 0 ? dl0[0] : (mw == 1 ? dl0[1] : dl0[NWG - 1]);
+#pragma unroll
+                for (int ks = 0; ks < TM / 16; ++ks) mma_f16(xg, dh + 16 * ks, dh + 16 * ks, idesc1, ks > 0 ? 1u : 0u);
                 if (NPASS == 2) {
 #pragma unroll
                     for (int ks = 0; ks < TM / 16; ++ks) {
-                        const uint64_t dh = sdesc(h0 + ks * 256, 128, GRP);
-                        const uint64_t dl = sdesc(l0 + ks * 256, 128, GRP);
-                        mma_f16(xg, dl, dh, idesc2a, 1u);
-                        mma_f16(xg + TM, dl, sdesc(h0 + 18 * GRP + ks * 256, 128, GRP), idesc2b, 1u);
+                        mma_f16(xg, dl + 16 * ks, dh + 16 * ks, idesc2a, 1u);
+                        mma_f16(xg + TM, dl + 16 * ks, dh + (18 * GRP >> 4) + 16 * ks, idesc2b, 1u);
                     }
                 }
                 commit(&S.mdone[mw]);
             };
-            // issue whichever of the next E-step / next Gram is ready, E first: the
-            // warpgroups' critical path runs through E, the Gram only has to keep up
+            // The tensor pipe runs MMAs in issue order and the issuing thread blocks once a
+            // few are queued, so a Gram issued just before an E-step becomes ready delays the
+            // warpgroups' E -> U read -> E chain.  Policy 0 (default): whichever is ready, E
+            // first.  Policy P > 0: a Gram only right after an E-step, once every E-step is
+            // out, or after P clocks without one (a warpgroup draining its Gram to recentre
+            // waits for it before it releases the next E-step).  Measured (scripts/em_trace.py):
+            // the warpgroups' own per-tile work (~3.4k clocks per warpgroup and tile) is the
+            // critical path, and delaying Grams makes their flushes wait (P = 2000: 4.1 ms
+            // per 2^26-event pass against 3.6 ms).
+            const uint64_t dbh = sdesc(su32(S.bw[0]), 128, 256), dbl = sdesc(su32(S.bw[1]), 128, 256);
+            const uint64_t dbb = sdesc(su32(S.bb), 128, 256);
             int64_t je = 0, jm = 0;
+            long long tle = clock64();
             while (jm < J) {
-                bool did = false;
-                if (je < J && mbar_test(&S.aeready[je & 1], (uint32_t)((je >> 1) & 1)) &&
+                bool didE = false;
+                if (je < J && mbar_test(&S.aeready[je % NWG], (uint32_t)((je / NWG) & 1)) &&
                     (je == 0 || mbar_test(&S.efree, (uint32_t)((je - 1) & 1)))) {
-                    const int w = (int)(je & 1);
+                    const int w = (int)(je % NWG);
+                    TRACE(1, je);
                     tc_fence_after();
                     const uint32_t tah = tmem + TA0 + 16 * w, tal = tah + 8;
                     mma_f16_ta(tmem, tah, dbh, kIdescE, 0u);
@@ -497,22 +570,27 @@ __global__ void __launch_bounds__(NTHR, 1) k_em_mma(const __grid_constant__ CUte
                     mma_f16_ta(tmem, tal, dbh, kIdescE, 1u);
                     mma_f16_ta(tmem, tmem + TONE, dbb, kIdescE, 1u);
                     commit(&S.edone[w]);
+                    TRACE(9, je);
                     ++je;
-                    did = true;
+                    didE = true;
+                    tle = clock64();
                 }
-                if (jm < je && mbar_test(&S.mready[jm & 1], (uint32_t)((jm >> 1) & 1))) {
+                if ((policy == 0 || didE || je == J || clock64() - tle > policy) && jm < je &&
+                    mbar_test(&S.mready[jm % NWG], (uint32_t)((jm / NWG) & 1)) &&
+                    (jm < 2 || mbar_test(&S.rfree[jm & 1], (uint32_t)(((jm - 2) >> 1) & 1)))) {
+                    TRACE(2, jm);
+                    tc_fence_after();
                     gram(jm);
+                    TRACE(10, jm);
                     ++jm;
-                    did = true;
                 }
-                if (!did) __nanosleep(32);
             }
         }
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (warp == 9) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    if (warp == WMMA) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 bool em_mma_enabled() {
@@ -534,18 +612,42 @@ int em_mma_passes() {
     return v;
 }
 
-template <int NPASS, bool F32>
+// ES_EM_MMA_POLICY: MMA issue policy (0 default: whichever is ready; P > 0: a Gram right
+// after an E-step, or after P clocks without one)
+static int em_mma_policy() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ES_EM_MMA_POLICY");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
+}
+
+template <int NPASS, bool F32, int NWG>
 static void launch_npass(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model,
                          const double* center, double xs, const NegCx& ncx, double* partial, int grid,
                          cudaStream_t s) {
-    const size_t smem = sizeof(Smem<NPASS>) + 128;
+    const size_t smem = sizeof(Smem<NPASS, NWG>) + 128;
     static bool a = false;
     if (!a) {
-        cudaFuncSetAttribute(k_em_mma<NPASS, F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_em_mma<NPASS, F32, NWG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         a = true;
     }
-    k_em_mma<NPASS, F32><<<grid, NTHR, smem, s>>>(*xmap, n, D, K, model, center, xs, ncx,
-                                                   make_float2((float)xs, 0.f), partial);
+    NegCxF ncxf{};
+    for (int j = 0; j < DM; ++j) ncxf.v[j] = (float)ncx.v[j];
+    k_em_mma<NPASS, F32, NWG><<<grid, nthr(NWG), smem, s>>>(*xmap, n, D, K, model, center, xs, ncx, ncxf,
+                                                             (float)xs, em_mma_policy(), partial);
+}
+
+// ES_EM_MMA_WG=3 runs the NPASS = 1 kernel with three epilogue warpgroups (128 registers
+// per thread) instead of two; measured no faster (3.68-3.75 against 3.60-3.66 ms per pass).
+static int em_mma_wgs() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ES_EM_MMA_WG");
+        v = (e && e[0] == '3') ? 3 : 2;
+    }
+    return v;
 }
 
 void launch_em_mma(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model, const double* center,
@@ -563,15 +665,26 @@ void launch_em_mma(const CUtensorMap* xmap, int64_t n, int D, int K, const doubl
     const int grid = (int)std::min<int64_t>(num_sms, std::max<int64_t>(ntiles, 1));
     *nblk = grid;
     if (em_mma_passes() != 0) npass = em_mma_passes();
-    if (npass == 1 && f32conv)
-        launch_npass<1, true>(xmap, n, D, K, model, center, xs, ncx, partial, grid, s);
+    const bool w3 = em_mma_wgs() == 3;
+    if (npass == 1 && f32conv && w3)
+        launch_npass<1, true, 3>(xmap, n, D, K, model, center, xs, ncx, partial, grid, s);
+    else if (npass == 1 && f32conv)
+        launch_npass<1, true, 2>(xmap, n, D, K, model, center, xs, ncx, partial, grid, s);
+    else if (npass == 1 && w3)
+        launch_npass<1, false, 3>(xmap, n, D, K, model, center, xs, ncx, partial, grid, s);
     else if (npass == 1)
-        launch_npass<1, false>(xmap, n, D, K, model, center, xs, ncx, partial, grid, s);
+        launch_npass<1, false, 2>(xmap, n, D, K, model, center, xs, ncx, partial, grid, s);
     else if (f32conv)
-        launch_npass<2, true>(xmap, n, D, K, model, center, xs, ncx, partial, grid, s);
+        launch_npass<2, true, 2>(xmap, n, D, K, model, center, xs, ncx, partial, grid, s);
     else
-        launch_npass<2, false>(xmap, n, D, K, model, center, xs, ncx, partial, grid, s);
+        launch_npass<2, false, 2>(xmap, n, D, K, model, center, xs, ncx, partial, grid, s);
     ++ls.launches;
 }
 
 }  // namespace es
+
+#ifdef ES_EM_TRACE
+extern "C" int es_debug_em_trace(long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, es::g_em_trace, sizeof(es::g_em_trace));
+}
+#endif

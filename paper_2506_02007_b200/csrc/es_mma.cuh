@@ -30,6 +30,9 @@ constexpr uint32_t kIdescE = idesc_f16(128, 128, 0);
 struct NegCx {
     double v[DM];
 };
+struct NegCxF {  // the same rounded to FP32 (FP32-pipe conversion)
+    float v[DM];
+};
 
 // byte offset of (row, k) in a K-major 128 x 16 fp16 operand (SWIZZLE_NONE core matrices)
 __device__ __forceinline__ uint32_t kmaj(int row, int k) {
