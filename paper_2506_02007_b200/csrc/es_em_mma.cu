@@ -138,10 +138,10 @@ __global__ void __launch_bounds__(nthr(NWG), 1) k_em_mma(const __grid_constant__
     if (t == 0) {
         for (int i = 0; i < XS; ++i) {
             mbar_init(&S.xfull[i], 1);
-            mbar_init(&S.xfree[i], 1);
+            mbar_init(&S.xfree[i], 4);
         }
         for (int i = 0; i < NWG; ++i) {
-            mbar_init(&S.aeready[i], 1);
+            mbar_init(&S.aeready[i], 4);
             mbar_init(&S.edone[i], 1);
             mbar_init(&S.mready[i], 4);
             mbar_init(&S.mdone[i], 1);
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(nthr(NWG), 1) k_em_mma(const __grid_constant__
             named_sync(4 + w, 128);
         };
 
-        bool pend = false;   // the Gram of this WG's previous tile is still to be flushed
+        int64_t pendt = -1;  // last local tile whose Gram is not flushed yet
         int64_t jj = 0;      // local tile index
         // convert tile j: x^ = (x - c) xs -> FP32 row (registers) + fp16 hi/lo E-step A operand
         // in this WG's TMEM columns (lane = event, tcgen05.st)
@@ -311,12 +311,12 @@ __global__ void __launch_bounds__(nthr(NWG), 1) k_em_mma(const __grid_constant__
             tmem_st8(tmem + lq + TA0 + 16 * w + 8, lw);
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
-            named_sync(1 + w, 128);
-            if (p == 0) {
+            __syncwarp();
+            if (lane == 0) {  // per warp: its 32 events are read and staged
                 arrive(&S.xfree[s]);
                 arrive(&S.aeready[w]);
-                TRACE(5, j);
             }
+            if (p == 0) TRACE(5, j);
         };
         uint64_t x2[DM / 2], x2n[DM / 2];
         if (w < J) convert(w, x2);
@@ -380,9 +380,11 @@ __global__ void __launch_bounds__(nthr(NWG), 1) k_em_mma(const __grid_constant__
             }
             if (valid) cacc(llh, lll, ll);
             // ---- records (buffers w are free once the Gram of the previous tile completed)
-            if (pend) {
-                flush(jj - 1);
-                pend = false;
+            // (Accumulating two tiles' Grams in TMEM before a flush doubles the FP32
+            // truncation bias and fails the 2^25-event parity test; measured no faster.)
+            if (pendt >= 0) {
+                flush(pendt);
+                pendt = -1;
             }
             unsigned char* rh = S.rech[w] + (p >> 3) * 128 + (p & 7) * 16;
             unsigned char* rl = S.recl[NPASS == 2 ? w : 0] + (p >> 3) * 128 + (p & 7) * 16;
@@ -438,11 +440,11 @@ __global__ void __launch_bounds__(nthr(NWG), 1) k_em_mma(const __grid_constant__
             __syncwarp();
             if (lane == 0) arrive(&S.mready[w]);
             if (p == 0) TRACE(8, j);
-            pend = true;
+            pendt = jj;
             // recentre after local tiles 1, 2, 4, 8, ... (drain this WG's Gram first)
             if (((jj + 1) & jj) == 0 && j + NWG < J) {
                 flush(jj);
-                pend = false;
+                pendt = -1;
                 recentre(false);
             }
             if (LATE) {
@@ -452,7 +454,7 @@ __global__ void __launch_bounds__(nthr(NWG), 1) k_em_mma(const __grid_constant__
                 for (int r = 0; r < DM / 2; ++r) x2[r] = x2n[r];
             }
         }
-        if (pend) flush(jj - 1);
+        if (pendt >= 0) flush(pendt);
         recentre(true);
         // -------------------------------------------------------------- output
         // Sum the WGs' statistics (fixed order) about the starting centre
