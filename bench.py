@@ -300,8 +300,9 @@ def run_ours(args):
                      "algorithmic_bytes_per_launch": bytes_iter / world, "avg_launch_ms": em_kern_avg,
                      "kernel_share_of_step": kern_ms / em_ms if em_ms else None,
                      "traffic_source": args.traffic_note,
-                     "limiter": "shared-memory operand bandwidth of the block-diagonal Gram (tensor-core "
-                                "smem reads + record stores ~= 128 B/clk/SM) - see DESIGN.md section 3"},
+                     "limiter": "latency of the epilogue warpgroups' per-tile chain (U read, convert, softmax, "
+                                "flush, records ~3.9k clk per warpgroup-tile) and the single TMEM E region; no unit "
+                                "saturated (issue 49%, tensor 47%) - profiles/r01_k_em_mma_pipeline_trace.txt"},
         "score": {"events_per_s": sc_evs, "ms_per_pass": sc_ms / args.steps, "n_flagged": nflag,
                   "roofline": {"bound": "hbm", "kernel": sc_kernel, "achieved": sc_ach, "peak": hbm,
                                "unit": "GB/s", "frac": sc_ach / hbm,
@@ -325,7 +326,7 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override N (debug only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--traffic", type=float, default=8590171000.0 + 8156928.0,
+    ap.add_argument("--traffic", type=float, default=8591338000.0 + 4376064.0,
                     help="dram bytes per EM launch from the committed ncu --set full capture (profiles/)")
     ap.add_argument("--traffic-note", default="dram__bytes_read.sum + dram__bytes_write.sum of k_em_mma<1> at N=2^26, "
                                               "profiles/r01_k_em_mma1_ncu_summary.txt")
