@@ -18,6 +18,8 @@
  *   es_gmm_calibrate         <- calibrate_threshold
  *   es_gmm_select_k_bic      <- select_k_bic
  *   es_run_pipeline          <- run_pipeline
+ *   es_kmeans_baseline       <- kmeans_baseline
+ *   es_confusion             <- confusion
  *
  * Conventions
  *  - Plain pointers and sizes only.  Parameters are host FP64 arrays, row-major:
@@ -204,6 +206,18 @@ int es_run_pipeline(es_ctx* ctx, es_dataset* ds, const es_pipeline_cfg* cfg, es_
                     int32_t* best_k /* n_local, nullable */, double* best_logdens /* n_local, nullable */,
                     int64_t* anomaly_indices /* n_local capacity, nullable */, int64_t* n_local_flagged,
                     int64_t* n_flagged);
+
+/* eval-bench.  k-means baseline: k-means++ seeding (seed) and Lloyd's
+ * algorithm on the train split (first floor(train_window N) rows), stopping when no
+ * assignment changes or after max_iter steps (<= 0: 100); score = Euclidean distance to
+ * the nearest centroid; threshold = (1-q)-quantile of the train scores; flag iff score >
+ * threshold.  D <= 64.  Errors: TooFewPoints (n_train < K), RangeViolation. */
+int es_kmeans_baseline(es_ctx* ctx, es_dataset* ds, int32_t K, double q, double train_window, uint64_t seed,
+                       int32_t max_iter, double* centroids /* K*D, nullable */, double* threshold,
+                       uint8_t* flags /* n_local, nullable */, double* scores /* n_local, nullable */,
+                       int64_t* n_flagged, int32_t* iterations);
+/* out = {tp, fp, tn, fn}, anomaly = positive class; labels / flags host or device. */
+int es_confusion(es_ctx* ctx, const uint8_t* labels, const uint8_t* flags, int64_t n, int64_t* out);
 
 #ifdef __cplusplus
 }

@@ -593,6 +593,110 @@ int eso_calibrate(const double* X, int64_t n_train, int D, const double* pi, con
     return kOk;
 }
 
+
+// k-means baseline (eval-bench): k-means++ seeding as fit_em's, Lloyd's
+// algorithm on the train split (first floor(train_window N) rows) until no assignment
+// changes or max_iter steps (<= 0: 100); empty clusters keep their centroid; distance
+// squared as an FMA chain over features in order (ties -> lowest k); score = distance;
+// threshold = (1-q)-quantile of train scores (h = (n_train-1)(1-q), linear interpolation);
+// flag iff score > threshold.
+int eso_kmeans_baseline(const double* X, int64_t N, int D, int K, double q, double train_window, uint64_t seed,
+                        int max_iter, double* centroids, double* threshold, uint8_t* flags, double* scores,
+                        int64_t* n_flagged, int* iterations, int nthreads) {
+    if (K < 1) return fail(kData, "InvalidK", "K must be >= 1");
+    if (!(q > 0.0 && q < 1.0)) return fail(kData, "RangeViolation", "q must be in (0,1)");
+    if (!(train_window > 0.0 && train_window <= 1.0))
+        return fail(kData, "RangeViolation", "train_window must be in (0,1]");
+    const int64_t nt = (int64_t)std::floor(train_window * (double)N);
+    if (nt < K) return fail(kData, "TooFewPoints", "training split has fewer rows than K");
+    if (max_iter <= 0) max_iter = 100;
+    set_threads(nthreads);
+    SplitMix64 rng(seed);
+    std::vector<int64_t> rows;
+    kmeanspp_rows(X, nt, D, K, rng, rows);
+    std::vector<double> cen((size_t)K * D);
+    for (int k = 0; k < K; ++k)
+        for (int a = 0; a < D; ++a) cen[(size_t)k * D + a] = X[(size_t)rows[k] * D + a];
+    auto nearest = [&](const double* x, double* best) {
+        double b = INFINITY;
+        int bk = 0;
+        for (int k = 0; k < K; ++k) {
+            double d2 = 0.0;
+            for (int a = 0; a < D; ++a) {
+                const double e = x[a] - cen[(size_t)k * D + a];
+                d2 = std::fma(e, e, d2);
+            }
+            if (d2 < b) {
+                b = d2;
+                bk = k;
+            }
+        }
+        *best = b;
+        return bk;
+    };
+    std::vector<int> asg(nt, -1);
+    int it = 0;
+    while (it < max_iter) {
+        int64_t changed = 0;
+#pragma omp parallel for schedule(static) reduction(+ : changed)
+        for (int64_t i = 0; i < nt; ++i) {
+            double b;
+            const int k = nearest(X + (size_t)i * D, &b);
+            if (asg[i] != k) ++changed;
+            asg[i] = k;
+        }
+        std::vector<double> sum((size_t)K * D, 0.0), cnt(K, 0.0);
+        for (int64_t i = 0; i < nt; ++i) {
+            const int k = asg[i];
+            cnt[k] += 1.0;
+            for (int a = 0; a < D; ++a) sum[(size_t)k * D + a] += X[(size_t)i * D + a];
+        }
+        ++it;
+        for (int k = 0; k < K; ++k)
+            if (cnt[k] > 0.0)
+                for (int a = 0; a < D; ++a) cen[(size_t)k * D + a] = sum[(size_t)k * D + a] / cnt[k];
+        if (changed == 0) break;
+    }
+    std::vector<double> sc(N);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < N; ++i) {
+        double b;
+        nearest(X + (size_t)i * D, &b);
+        sc[i] = std::sqrt(b);
+    }
+    std::vector<double> v(sc.begin(), sc.begin() + nt);
+    const double h = (double)(nt - 1) * (1.0 - q);
+    const int64_t lo = (int64_t)std::floor(h);
+    const int64_t hi = std::min<int64_t>(lo + 1, nt - 1);
+    std::nth_element(v.begin(), v.begin() + lo, v.end());
+    const double vlo = v[lo];
+    double vhi = vlo;
+    if (hi != lo) vhi = *std::min_element(v.begin() + lo + 1, v.end());
+    const double thr = vlo + (h - (double)lo) * (vhi - vlo);
+    int64_t nf = 0;
+    for (int64_t i = 0; i < N; ++i) {
+        const uint8_t f = sc[i] > thr ? 1 : 0;
+        if (flags) flags[i] = f;
+        nf += f;
+    }
+    if (scores) std::copy(sc.begin(), sc.end(), scores);
+    if (centroids) std::copy(cen.begin(), cen.end(), centroids);
+    *threshold = thr;
+    *n_flagged = nf;
+    *iterations = it;
+    return kOk;
+}
+
+// confusion: out = {tp, fp, tn, fn}, anomaly = positive class
+int eso_confusion(const uint8_t* labels, const uint8_t* flags, int64_t n, int64_t* out) {
+    out[0] = out[1] = out[2] = out[3] = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        const int l = labels[i] != 0, f = flags[i] != 0;
+        ++out[l ? (f ? 0 : 3) : (f ? 1 : 2)];
+    }
+    return kOk;
+}
+
 int eso_select_k_bic(const double* X, int64_t N, int D, const int* k_range, int n_k, const eso_fit_opts* opts,
                      int* best_k, double* bic) {
     if (n_k < 1) return fail(kData, "EmptyRange", "k_range is empty");

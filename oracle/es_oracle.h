@@ -89,6 +89,10 @@ int eso_detect(const double* X, int64_t N, int D, const double* pi, const double
 
 /* calibrate_threshold: q-quantile (linear interpolation between
  * order statistics, h = (n-1) q) of best-component densities over rows [0,n_train). */
+int eso_kmeans_baseline(const double* X, int64_t N, int D, int K, double q, double train_window, uint64_t seed,
+                        int max_iter, double* centroids, double* threshold, uint8_t* flags, double* scores,
+                        int64_t* n_flagged, int* iterations, int nthreads);
+int eso_confusion(const uint8_t* labels, const uint8_t* flags, int64_t n, int64_t* out);
 int eso_calibrate(const double* X, int64_t n_train, int D, const double* pi,
                   const double* mu, const double* cov, int K, double q, int mode,
                   double* delta, double* log_delta, int nthreads);

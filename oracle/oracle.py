@@ -178,6 +178,31 @@ def calibrate(X_train, pi, mu, cov, q, mode=0, nthreads=0):
     return d.value, ld.value
 
 
+def kmeans_baseline(X, K, q=0.01, train_window=0.5, seed=0, max_iter=100, nthreads=0):
+    """SPEC.md:451-458 restated (es_oracle.cpp eso_kmeans_baseline)."""
+    X = np.ascontiguousarray(X, np.float64)
+    N, D = X.shape
+    cen = np.empty((K, D))
+    flags = np.empty(N, np.uint8)
+    scores = np.empty(N)
+    thr, nf, it = C.c_double(), C.c_int64(), C.c_int()
+    _check(lib().eso_kmeans_baseline(_p(X), C.c_int64(N), D, K, C.c_double(q), C.c_double(train_window),
+                                     C.c_uint64(seed), max_iter, _p(cen), C.byref(thr), _p(flags), _p(scores),
+                                     C.byref(nf), C.byref(it), nthreads))
+    return cen, thr.value, flags, scores, nf.value, it.value
+
+
+def confusion(labels, flags):
+    """SPEC.md:431-437: (tp, fp, tn, fn), anomaly = positive class."""
+    lab = np.ascontiguousarray(labels, np.uint8)
+    fl = np.ascontiguousarray(flags, np.uint8)
+    if lab.shape != fl.shape:
+        raise OracleError(1, "LengthMismatch", "labels and flags differ in length")
+    out = np.zeros(4, np.int64)
+    _check(lib().eso_confusion(_p(lab), _p(fl), C.c_int64(lab.size), _p(out)))
+    return tuple(int(v) for v in out)
+
+
 def select_k_bic(X, k_range, init="kmeans++", tol=1e-6, max_iter=200, reg=None, seed=0, nthreads=0,
                  covariance_type="full"):
     X = np.ascontiguousarray(X, np.float64)

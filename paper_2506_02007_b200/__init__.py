@@ -538,3 +538,119 @@ def run_pipeline(X, K: int, train_window: float = 0.5, quantile_q: Optional[floa
     model = GmmModel(w, mu, cov, fr)
     report = DetectionReport(fl, idx[:nloc.value].copy(), bk, bl, model, d.value, ld.value, ng.value)
     return PipelineResult(model, report, mean, scale, int(np.floor(train_window * ds.n_global)))
+
+
+# ------------------------------------------------------------------ eval-bench
+@dataclass
+class KMeansResult:
+    """kmeans_baseline: centroids fitted on the train split, the
+    (1-q)-quantile threshold of the train distances, per-event distances and flags."""
+    centroids: np.ndarray
+    threshold: float
+    flags: np.ndarray
+    scores: np.ndarray
+    n_flagged: int
+    iterations: int
+
+
+def kmeans_baseline(X, K: int, q: float = 0.01, train_window: float = 0.5, seed: int = 0, max_iter: int = 100,
+                    ctx: Optional[Context] = None) -> KMeansResult:
+    """KMeans baseline on the device (es_kmeans_baseline): k-means++ seeding and Lloyd's
+    algorithm on the first train_window fraction of the events; flag iff the distance to
+    the nearest centroid exceeds the (1-q)-quantile of the train distances."""
+    ds = _as_dataset(X, ctx)
+    D, n = ds.D, ds.n_local
+    cen = np.empty((K, D))
+    fl, sc = np.empty(n, np.uint8), np.empty(n)
+    thr, nf, it = C.c_double(), C.c_int64(), C.c_int32()
+    _check(ds.ctx._lib.es_kmeans_baseline(ds.ctx.handle, ds.handle, C.c_int32(K), C.c_double(q),
+                                          C.c_double(train_window), C.c_uint64(seed), C.c_int32(max_iter),
+                                          C.c_void_p(cen.ctypes.data), C.byref(thr), C.c_void_p(_ptr(fl)),
+                                          C.c_void_p(_ptr(sc)), C.byref(nf), C.byref(it)))
+    return KMeansResult(cen, thr.value, fl, sc, nf.value, it.value)
+
+
+@dataclass
+class ConfusionMatrix:
+    """counts with anomaly as the positive class."""
+    tp: int
+    fp: int
+    tn: int
+    fn: int
+
+
+def confusion(labels, flags, ctx: Optional[Context] = None) -> ConfusionMatrix:
+    """confusion(labels, flags) (SPEC.md:431-437), counted on the device (es_confusion);
+    labels / flags may be host arrays or device tensors of equal length."""
+    c = ctx or default_context()
+    nl, nf = len(labels), len(flags)
+    if nl != nf:
+        raise EventscopeError("Data", "LengthMismatch", f"labels ({nl}) and flags ({nf}) differ in length")
+    lab = labels if hasattr(labels, "data_ptr") else np.ascontiguousarray(labels, np.uint8)
+    fl = flags if hasattr(flags, "data_ptr") else np.ascontiguousarray(flags, np.uint8)
+    out = np.zeros(4, np.int64)
+    _check(c._lib.es_confusion(c.handle, C.c_void_p(_ptr(lab)), C.c_void_p(_ptr(fl)), C.c_int64(nl),
+                               C.c_void_p(out.ctypes.data)))
+    return ConfusionMatrix(*(int(v) for v in out))
+
+
+@dataclass
+class EvalSummary:
+    """SPEC.md:424-428."""
+    accuracy: float
+    precision: float
+    recall: float
+    f1: float
+    cm: ConfusionMatrix
+    method: str = "gmm"
+    params: tuple = ()
+
+
+def metrics(cm: ConfusionMatrix, method: str = "gmm", params: tuple = ()) -> EvalSummary:
+    """metrics(cm): zero-division conventions fixed to 0."""
+    n = cm.tp + cm.fp + cm.tn + cm.fn
+    if n <= 0:
+        raise EventscopeError("Data", "EmptyMatrix", "confusion matrix has no events")
+    precision = cm.tp / (cm.tp + cm.fp) if cm.tp + cm.fp else 0.0
+    recall = cm.tp / (cm.tp + cm.fn) if cm.tp + cm.fn else 0.0
+    f1 = 2 * precision * recall / (precision + recall) if precision + recall else 0.0
+    return EvalSummary((cm.tp + cm.tn) / n, precision, recall, f1, cm, method, params)
+
+
+def sensitivity_sweep(X, labels, K_range: Sequence[int], q_range: Sequence[float], seeds: Sequence[int] = (0,),
+                      layer: str = "all", csv_path: Optional[str] = None, ctx: Optional[Context] = None,
+                      **pipeline_kw):
+    """sensitivity_sweep: the full K x q grid of run_pipeline cells, each
+    averaged over seeds; a failing cell is recorded in the grid (status = error name), not
+    raised.  The feature matrix is uploaded once and shared by every cell.  Returns rows
+    with the CSV columns layer, K, q, seed_count, accuracy, precision, recall, f1, status
+    (and writes them to csv_path when given)."""
+    if not len(K_range) or not len(q_range) or not len(seeds):
+        raise EventscopeError("Data", "EmptyRange", "K_range, q_range and seeds must be nonempty")
+    ds = _as_dataset(X, ctx)
+    lab = np.ascontiguousarray(labels, np.uint8)
+    rows = []
+    for K in K_range:
+        for q in q_range:
+            acc = []
+            status = "ok"
+            for sd in seeds:
+                try:
+                    r = run_pipeline(ds, int(K), quantile_q=float(q), seed=int(sd), **pipeline_kw)
+                    acc.append(metrics(confusion(lab, r.report.flags, ds.ctx), "gmm", (int(K), float(q))))
+                except EventscopeError as e:
+                    status = e.name
+            if acc:
+                m = [float(np.mean([getattr(a, f) for a in acc])) for f in ("accuracy", "precision", "recall", "f1")]
+            else:
+                m = [float("nan")] * 4
+            rows.append({"layer": layer, "K": int(K), "q": float(q), "seed_count": len(acc), "accuracy": m[0],
+                         "precision": m[1], "recall": m[2], "f1": m[3], "status": status})
+    if csv_path:
+        import csv as _csv
+        with open(csv_path, "w", newline="") as fh:
+            w = _csv.DictWriter(fh, fieldnames=["layer", "K", "q", "seed_count", "accuracy", "precision", "recall",
+                                                "f1", "status"])
+            w.writeheader()
+            w.writerows(rows)
+    return rows

@@ -1470,4 +1470,169 @@ void launch_kpp_update(const double* X, int64_t n, int64_t ld, int D, const doub
     ++ls.launches;
 }
 
+
+// ------------------------------------------------------------------ k-means baseline
+// (eval-bench kmeans_baseline).  Rows in fixed order: CTA b, warp w,
+// lane l take row (b + gridDim.x * it) * (32 * nwarps) + 32 w + l.  Nearest centroid by
+// squared Euclidean distance as an FMA chain over the features in order (the oracle
+// uses the same chain), ties -> lowest k.  Mode 0 (Lloyd step): per centroid the sum of
+// its rows and their count, and the number of changed assignments, reduced per warp with
+// xor shuffles and per CTA in warp order -> partial[blk][K (D + 1) + 1]; mode 1: the
+// distance to the nearest centroid of every row.
+__device__ __forceinline__ double warp_allsum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <int DM>
+__global__ void __launch_bounds__(kBlock) k_lloyd(const double* __restrict__ X, int64_t n, int64_t ld, int D, int K,
+                                                  const double* __restrict__ cen, int32_t* __restrict__ assign,
+                                                  double* __restrict__ partial, double* __restrict__ score, int mode) {
+    extern __shared__ double sm[];
+    const int L = K * (D + 1) + 1, nw = kBlock / 32;
+    double* sc = sm;           // centroids [K][D]
+    double* acc = sm + K * D;  // [nw][L]
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    for (int e = t; e < K * D; e += kBlock) sc[e] = cen[e];
+    if (mode == 0)
+        for (int e = t; e < nw * L; e += kBlock) acc[e] = 0.0;
+    __syncthreads();
+    double* wa = acc + warp * L;
+    const int64_t step = (int64_t)gridDim.x * kBlock;
+    for (int64_t base = (int64_t)blockIdx.x * kBlock; base < n; base += step) {
+        const int64_t i = base + warp * 32 + lane;
+        const bool valid = i < n;
+        double x[DM];
+#pragma unroll
+        for (int a = 0; a < DM; ++a) x[a] = (valid && a < D) ? X[(int64_t)a * ld + i] : 0.0;
+        double best = INFINITY;
+        int bk = 0;
+        for (int k = 0; k < K; ++k) {
+            double d2 = 0.0;
+#pragma unroll
+            for (int a = 0; a < DM; ++a) {
+                if (a < D) {
+                    const double e = x[a] - sc[k * D + a];
+                    d2 = fma(e, e, d2);
+                }
+            }
+            if (d2 < best) {
+                best = d2;
+                bk = k;
+            }
+        }
+        if (mode == 1) {
+            if (valid) score[i] = sqrt(best);
+            continue;
+        }
+        const bool ch = valid && assign[i] != bk;
+        if (valid) assign[i] = bk;
+        const unsigned chb = __ballot_sync(0xffffffffu, ch);
+        for (int k = 0; k < K; ++k) {
+            const bool m = valid && bk == k;
+            const unsigned mb = __ballot_sync(0xffffffffu, m);
+            if (!mb) continue;
+#pragma unroll
+            for (int a = 0; a < DM; ++a) {
+                if (a < D) {
+                    const double v = warp_allsum(m ? x[a] : 0.0);
+                    if (lane == 0) wa[k * (D + 1) + a] += v;
+                }
+            }
+            if (lane == 0) wa[k * (D + 1) + D] += (double)__popc(mb);
+        }
+        if (lane == 0) wa[L - 1] += (double)__popc(chb);
+    }
+    if (mode == 0) {
+        __syncthreads();
+        for (int e = t; e < L; e += kBlock) {
+            double v = 0.0;
+            for (int w = 0; w < nw; ++w) v += acc[w * L + e];
+            partial[(int64_t)blockIdx.x * L + e] = v;
+        }
+    }
+}
+
+template <int DM>
+static void lloyd_dm(const double* X, int64_t n, int64_t ld, int D, int K, const double* cen, int32_t* assign,
+                     double* partial, double* score, int mode, int grid, cudaStream_t s) {
+    const size_t smem = (size_t)(K * D + (kBlock / 32) * (K * (D + 1) + 1)) * sizeof(double);
+    static size_t set = 0;
+    if (smem > 48 * 1024 && smem > set) {
+        cudaFuncSetAttribute(k_lloyd<DM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        set = smem;
+    }
+    k_lloyd<DM><<<grid, kBlock, smem, s>>>(X, n, ld, D, K, cen, assign, partial, score, mode);
+}
+
+int lloyd_grid(int64_t n, int num_sms) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>(num_sms, (n + kBlock - 1) / kBlock));
+}
+
+void launch_lloyd(const double* X, int64_t n, int64_t ld, int D, int K, const double* cen, int32_t* assign,
+                  double* partial, double* score, int mode, int grid, cudaStream_t s, LaunchStats& ls) {
+    if (n <= 0) return;
+    if (D <= 8)
+        lloyd_dm<8>(X, n, ld, D, K, cen, assign, partial, score, mode, grid, s);
+    else if (D <= 16)
+        lloyd_dm<16>(X, n, ld, D, K, cen, assign, partial, score, mode, grid, s);
+    else if (D <= 32)
+        lloyd_dm<32>(X, n, ld, D, K, cen, assign, partial, score, mode, grid, s);
+    else
+        lloyd_dm<64>(X, n, ld, D, K, cen, assign, partial, score, mode, grid, s);
+    ++ls.launches;
+}
+
+// flag_i = score_i > threshold; per-CTA flag counts
+__global__ void k_flag_gt(const double* __restrict__ score, int64_t n, double thr, uint8_t* __restrict__ flags,
+                          unsigned long long* __restrict__ count) {
+    __shared__ unsigned long long c;
+    if (threadIdx.x == 0) c = 0;
+    __syncthreads();
+    unsigned long long mine = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint8_t f = score[i] > thr ? 1 : 0;
+        flags[i] = f;
+        mine += f;
+    }
+    atomicAdd(&c, mine);
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(count, c);
+}
+
+void launch_flag_gt(const double* score, int64_t n, double thr, uint8_t* flags, unsigned long long* count,
+                    int num_sms, cudaStream_t s, LaunchStats& ls) {
+    cudaMemsetAsync(count, 0, sizeof(unsigned long long), s);
+    if (n <= 0) return;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(4 * num_sms, (n + kBlock - 1) / kBlock));
+    k_flag_gt<<<grid, kBlock, 0, s>>>(score, n, thr, flags, count);
+    ++ls.launches;
+}
+
+// confusion counts (anomaly = positive): out[0..3] = tp, fp, tn, fn
+__global__ void k_confusion(const uint8_t* __restrict__ labels, const uint8_t* __restrict__ flags, int64_t n,
+                            unsigned long long* __restrict__ out) {
+    __shared__ unsigned long long c[4];
+    if (threadIdx.x < 4) c[threadIdx.x] = 0;
+    __syncthreads();
+    unsigned long long m[4] = {0, 0, 0, 0};
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int l = labels[i] != 0, f = flags[i] != 0;
+        m[l ? (f ? 0 : 3) : (f ? 1 : 2)] += 1;
+    }
+    for (int j = 0; j < 4; ++j) atomicAdd(&c[j], m[j]);
+    __syncthreads();
+    if (threadIdx.x < 4) atomicAdd(&out[threadIdx.x], c[threadIdx.x]);
+}
+
+void launch_confusion(const uint8_t* labels, const uint8_t* flags, int64_t n, unsigned long long* out, int num_sms,
+                      cudaStream_t s, LaunchStats& ls) {
+    cudaMemsetAsync(out, 0, 4 * sizeof(unsigned long long), s);
+    if (n <= 0) return;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(4 * num_sms, (n + kBlock - 1) / kBlock));
+    k_confusion<<<grid, kBlock, 0, s>>>(labels, flags, n, out);
+    ++ls.launches;
+}
+
 }  // namespace es

@@ -131,4 +131,16 @@ void launch_score_fast(const double* X, int64_t n, int64_t ld, int D, int K, con
 void launch_synth(double* X, int64_t ld, int64_t n, int64_t grow0, int D, int K, const double* syn_model,
                   uint64_t seed, cudaStream_t s, LaunchStats& ls);
 
+
+// k-means baseline (eval-bench): Lloyd step (mode 0: partial[blk][K (D + 1) + 1] = per
+// centroid row sums | count, then changed assignments) or scoring (mode 1: score[i] =
+// distance to the nearest centroid), D <= 64; grid from lloyd_grid (fixed row order).
+int lloyd_grid(int64_t n, int num_sms);
+void launch_lloyd(const double* X, int64_t n, int64_t ld, int D, int K, const double* cen, int32_t* assign,
+                  double* partial, double* score, int mode, int grid, cudaStream_t s, LaunchStats& ls);
+void launch_flag_gt(const double* score, int64_t n, double thr, uint8_t* flags, unsigned long long* count,
+                    int num_sms, cudaStream_t s, LaunchStats& ls);
+void launch_confusion(const uint8_t* labels, const uint8_t* flags, int64_t n, unsigned long long* out, int num_sms,
+                      cudaStream_t s, LaunchStats& ls);
+
 }  // namespace es

@@ -542,6 +542,72 @@ double radix_select(es_ctx* c, const double* dkeys, int64_t n, int64_t r) {
 // ---------------------------------------------------------------- EM core
 bool is_diag(const es_em_state* st) { return st->opts.covariance_type == ES_COV_DIAG; }
 
+// k-means++ seeding on the device: first centre uniform; then D^2-weighted
+// draws, cumulative sum over global rows in chunk order (4096-row chunks).  Shared by
+// fit_em's KMeansPP init and the k-means baseline.
+std::vector<int64_t> kmeanspp_device(es_ctx* c, es_dataset* ds, int K, SplitMix64& rng) {
+    const int D = ds->D;
+    std::vector<int64_t> rows;
+    // k-means++ (DESIGN.md): first centre uniform; then D^2-weighted draws,
+    // cumulative sum over global rows in chunk order (4096-row chunks).
+    rows.push_back((int64_t)rng.below((uint64_t)ds->n_global));
+    const int64_t CH = 4096;
+    const int64_t nlc = (ds->n_local + CH - 1) / CH;
+    double* d2 = c->kpp.as<double>(std::max<int64_t>(ds->n_local, 1) + nlc + 8);
+    double* parts = d2 + std::max<int64_t>(ds->n_local, 1);
+    double* dcen = c->scratch2.as<double>(D);
+    std::vector<double> cen;
+    for (int j = 1; j < K; ++j) {
+        fetch_rows(c, ds, {rows.back()}, cen);
+        CU(cudaMemcpyAsync(dcen, cen.data(), D * 8, cudaMemcpyHostToDevice, c->stream));
+        launch_kpp_update(ds->X, ds->n_local, ds->ld, D, dcen, d2, parts, j == 1, c->stream, c->ls);
+        c->check_launch();
+        std::vector<double> hp(nlc);
+        if (nlc) CU(cudaMemcpyAsync(hp.data(), parts, nlc * 8, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        double loc = 0.0;
+        for (double v : hp) loc += v;
+        std::vector<double> all = c->allgather_host(&loc, 1);
+        double total = 0.0;
+        for (double v : all) total += v;
+        const double u = rng.uniform() * total;
+        int64_t pick = -1;
+        if (total > 0.0) {
+            // owner rank of the crossing point locates the row; others report -1
+            double before = 0.0;
+            for (int g = 0; g < c->rank; ++g) before += all[g];
+            double found = -1.0;
+            if (u >= before && u < before + all[c->rank]) {
+                double acc = before;
+                int64_t ch = 0;
+                for (; ch < nlc; ++ch) {
+                    if (acc + hp[ch] > u) break;
+                    acc += hp[ch];
+                }
+                if (ch == nlc) ch = nlc - 1;
+                const int64_t r0 = ch * CH, nr = std::min(CH, ds->n_local - r0);
+                std::vector<double> seg(nr);
+                CU(cudaMemcpyAsync(seg.data(), d2 + r0, nr * 8, cudaMemcpyDeviceToHost, c->stream));
+                c->sync();
+                int64_t li = r0 + nr - 1;
+                for (int64_t q = 0; q < nr; ++q) {
+                    acc += seg[q];
+                    if (acc > u) {
+                        li = r0 + q;
+                        break;
+                    }
+                }
+                found = (double)(ds->row_offset + li);
+            }
+            c->allreduce_host(&found, 1, 0, 2);
+            pick = (int64_t)found;
+        }
+        if (pick < 0) pick = (int64_t)rng.below((uint64_t)ds->n_global);
+        rows.push_back(pick);
+    }
+    return rows;
+}
+
 void em_init_model(es_em_state* st, const es_gmm_params* init, const DataStats& dsx) {
     es_ctx* c = st->ctx;
     es_dataset* ds = st->ds;
@@ -556,63 +622,7 @@ void em_init_model(es_em_state* st, const es_gmm_params* init, const DataStats& 
     } else {
         std::vector<int64_t> rows;
         if (st->opts.init == ES_INIT_KMEANSPP) {
-            // k-means++ (DESIGN.md): first centre uniform; then D^2-weighted draws,
-            // cumulative sum over global rows in chunk order (4096-row chunks).
-            rows.push_back((int64_t)st->rng.below((uint64_t)ds->n_global));
-            const int64_t CH = 4096;
-            const int64_t nlc = (ds->n_local + CH - 1) / CH;
-            double* d2 = c->kpp.as<double>(std::max<int64_t>(ds->n_local, 1) + nlc + 8);
-            double* parts = d2 + std::max<int64_t>(ds->n_local, 1);
-            double* dcen = c->scratch2.as<double>(D);
-            std::vector<double> cen;
-            for (int j = 1; j < K; ++j) {
-                fetch_rows(c, ds, {rows.back()}, cen);
-                CU(cudaMemcpyAsync(dcen, cen.data(), D * 8, cudaMemcpyHostToDevice, c->stream));
-                launch_kpp_update(ds->X, ds->n_local, ds->ld, D, dcen, d2, parts, j == 1, c->stream, c->ls);
-                c->check_launch();
-                std::vector<double> hp(nlc);
-                if (nlc) CU(cudaMemcpyAsync(hp.data(), parts, nlc * 8, cudaMemcpyDeviceToHost, c->stream));
-                c->sync();
-                double loc = 0.0;
-                for (double v : hp) loc += v;
-                std::vector<double> all = c->allgather_host(&loc, 1);
-                double total = 0.0;
-                for (double v : all) total += v;
-                const double u = st->rng.uniform() * total;
-                int64_t pick = -1;
-                if (total > 0.0) {
-                    // owner rank of the crossing point locates the row; others report -1
-                    double before = 0.0;
-                    for (int g = 0; g < c->rank; ++g) before += all[g];
-                    double found = -1.0;
-                    if (u >= before && u < before + all[c->rank]) {
-                        double acc = before;
-                        int64_t ch = 0;
-                        for (; ch < nlc; ++ch) {
-                            if (acc + hp[ch] > u) break;
-                            acc += hp[ch];
-                        }
-                        if (ch == nlc) ch = nlc - 1;
-                        const int64_t r0 = ch * CH, nr = std::min(CH, ds->n_local - r0);
-                        std::vector<double> seg(nr);
-                        CU(cudaMemcpyAsync(seg.data(), d2 + r0, nr * 8, cudaMemcpyDeviceToHost, c->stream));
-                        c->sync();
-                        int64_t li = r0 + nr - 1;
-                        for (int64_t q = 0; q < nr; ++q) {
-                            acc += seg[q];
-                            if (acc > u) {
-                                li = r0 + q;
-                                break;
-                            }
-                        }
-                        found = (double)(ds->row_offset + li);
-                    }
-                    c->allreduce_host(&found, 1, 0, 2);
-                    pick = (int64_t)found;
-                }
-                if (pick < 0) pick = (int64_t)st->rng.below((uint64_t)ds->n_global);
-                rows.push_back(pick);
-            }
+            rows = kmeanspp_device(c, ds, K, st->rng);
         } else {
             while ((int)rows.size() < K) {
                 const int64_t r = (int64_t)st->rng.below((uint64_t)ds->n_global);
@@ -1137,6 +1147,136 @@ int es_run_pipeline(es_ctx* c, es_dataset* ds, const es_pipeline_cfg* cfg, es_gm
         if (std_scale) std::copy(scale.begin(), scale.end(), std_scale);
     });
     return status;
+}
+
+// k-means baseline (eval-bench): Lloyd's algorithm with k-means++
+// seeding on the train split (the first floor(train_window N) rows, as run_pipeline);
+// score = distance to the nearest centroid; threshold = (1 - q)-quantile of the train
+// scores (linear interpolation, h = (n_train - 1)(1 - q), the calibrate convention);
+// flag iff score > threshold.  Lloyd stops when no assignment changes or after max_iter
+// steps; an empty cluster keeps its centroid.
+int es_kmeans_baseline(es_ctx* c, es_dataset* ds, int32_t K, double q, double train_window, uint64_t seed,
+                       int32_t max_iter, double* centroids, double* threshold, uint8_t* flags, double* scores,
+                       int64_t* n_flagged, int32_t* iterations) {
+    struct View {
+        es_dataset* v = nullptr;
+        ~View() {
+            if (v) v->X = nullptr;
+            delete v;
+        }
+    } V;
+    return guard([&] {
+        CU(cudaSetDevice(c->device));
+        const int D = ds->D;
+        if (K < 1) fail(ES_ERR_DATA, "InvalidK", "K must be >= 1");
+        if (D > 64) fail(ES_ERR_DATA, "DimensionTooLarge", "k-means baseline supports D <= 64");
+        if (!(q > 0.0 && q < 1.0)) fail(ES_ERR_DATA, "RangeViolation", "q must be in (0,1)");
+        if (!(train_window > 0.0 && train_window <= 1.0))
+            fail(ES_ERR_DATA, "RangeViolation", "train_window must be in (0,1]");
+        const int64_t n_train = (int64_t)std::floor(train_window * (double)ds->n_global);
+        if (n_train < K) fail(ES_ERR_DATA, "TooFewPoints", "training split has fewer rows than K");
+        if ((size_t)(K * D + 8 * (K * (D + 1) + 1)) * 8 > 227 * 1024)
+            fail(ES_ERR_DATA, "DimensionTooLarge", "K (D + 1) too large for the k-means kernel");
+        if (max_iter <= 0) max_iter = 100;
+        V.v = make_view(c, ds, ds->X, n_train);
+        es_dataset* tr = V.v;
+        SplitMix64 rng(seed);
+        const std::vector<int64_t> rows = kmeanspp_device(c, tr, K, rng);
+        std::vector<double> cen;
+        fetch_rows(c, tr, rows, cen);
+        const int L = K * (D + 1) + 1;
+        const int grid = lloyd_grid(tr->n_local, c->num_sms);
+        double* dcen = c->o1.as<double>((size_t)K * D);
+        int32_t* asg = c->o2.as<int32_t>(std::max<int64_t>(tr->n_local, 1));
+        double* part = c->o3.as<double>((size_t)grid * L);
+        double* red = c->o4.as<double>(L);
+        CU(cudaMemsetAsync(asg, 0xFF, std::max<int64_t>(tr->n_local, 1) * 4, c->stream));  // -1: unassigned
+        int it = 0;
+        std::vector<double> h(L);
+        while (it < max_iter) {
+            CU(cudaMemcpyAsync(dcen, cen.data(), (size_t)K * D * 8, cudaMemcpyHostToDevice, c->stream));
+            if (tr->n_local > 0) {
+                launch_lloyd(tr->X, tr->n_local, tr->ld, D, K, dcen, asg, part, nullptr, 0, grid, c->stream, c->ls);
+                c->check_launch();
+                launch_reduce_blocks(part, grid, L, red, c->stream, c->ls);
+                c->check_launch();
+                CU(cudaMemcpyAsync(h.data(), red, (size_t)L * 8, cudaMemcpyDeviceToHost, c->stream));
+                c->sync();
+            } else {
+                std::fill(h.begin(), h.end(), 0.0);
+            }
+            const std::vector<double> all = c->allgather_host(h.data(), L);  // rank-ordered sum
+            std::vector<double> tot(L, 0.0);
+            for (int g = 0; g < c->world; ++g)
+                for (int e = 0; e < L; ++e) tot[e] += all[(size_t)g * L + e];
+            ++it;
+            for (int k = 0; k < K; ++k) {
+                const double cnt = tot[(size_t)k * (D + 1) + D];
+                if (cnt > 0.0)
+                    for (int a = 0; a < D; ++a) cen[(size_t)k * D + a] = tot[(size_t)k * (D + 1) + a] / cnt;
+            }
+            if (tot[L - 1] == 0.0) break;  // no assignment changed: the centroids are the ones just used
+        }
+        // scores of every local row, threshold from the train rows, flags
+        CU(cudaMemcpyAsync(dcen, cen.data(), (size_t)K * D * 8, cudaMemcpyHostToDevice, c->stream));
+        double* dsc = c->out_scratch.as<double>(std::max<int64_t>(ds->n_local, 1));
+        launch_lloyd(ds->X, ds->n_local, ds->ld, D, K, dcen, nullptr, nullptr, dsc, 1,
+                     lloyd_grid(ds->n_local, c->num_sms), c->stream, c->ls);
+        c->check_launch();
+        const double hq = (double)(n_train - 1) * (1.0 - q);
+        const int64_t lo = (int64_t)std::floor(hq);
+        const int64_t hi = std::min<int64_t>(lo + 1, n_train - 1);
+        const int64_t nloc = tr->n_local;
+        const double vlo = radix_select(c, dsc, nloc, lo);
+        const double vhi = hi == lo ? vlo : radix_select(c, dsc, nloc, hi);
+        const double thr = vlo + (hq - (double)lo) * (vhi - vlo);
+        uint8_t* dfl = c->o5.as<uint8_t>(std::max<int64_t>(ds->n_local, 1));
+        unsigned long long* dcount = c->hist.as<unsigned long long>(256);
+        launch_flag_gt(dsc, ds->n_local, thr, dfl, dcount, c->num_sms, c->stream, c->ls);
+        c->check_launch();
+        unsigned long long cnt = 0;
+        CU(cudaMemcpyAsync(&cnt, dcount, 8, cudaMemcpyDeviceToHost, c->stream));
+        if (flags && ds->n_local)
+            CU(cudaMemcpyAsync(flags, dfl, ds->n_local, cudaMemcpyDefault, c->stream));
+        if (scores && ds->n_local)
+            CU(cudaMemcpyAsync(scores, dsc, ds->n_local * 8, cudaMemcpyDefault, c->stream));
+        c->sync();
+        double total = (double)cnt;
+        c->allreduce_host(&total, 1, 0, 0);
+        if (centroids) std::copy(cen.begin(), cen.end(), centroids);
+        if (threshold) *threshold = thr;
+        if (n_flagged) *n_flagged = (int64_t)total;
+        if (iterations) *iterations = it;
+    });
+}
+
+// confusion counts of labels against flags (anomaly = positive class);
+// host or device arrays; out = {tp, fp, tn, fn}
+int es_confusion(es_ctx* c, const uint8_t* labels, const uint8_t* flags, int64_t n, int64_t* out) {
+    return guard([&] {
+        CU(cudaSetDevice(c->device));
+        if (n < 0) fail(ES_ERR_DATA, "LengthMismatch", "negative length");
+        if (!out) fail(ES_ERR_DATA, "InvalidArgument", "null output");
+        const uint8_t* dl = labels;
+        const uint8_t* df = flags;
+        if (n > 0 && !is_device_ptr(labels)) {
+            uint8_t* t = c->o1.as<uint8_t>(n);
+            CU(cudaMemcpyAsync(t, labels, n, cudaMemcpyHostToDevice, c->stream));
+            dl = t;
+        }
+        if (n > 0 && !is_device_ptr(flags)) {
+            uint8_t* t = c->o2.as<uint8_t>(n);
+            CU(cudaMemcpyAsync(t, flags, n, cudaMemcpyHostToDevice, c->stream));
+            df = t;
+        }
+        unsigned long long* d = c->hist.as<unsigned long long>(256);
+        launch_confusion(dl, df, n, d, c->num_sms, c->stream, c->ls);
+        c->check_launch();
+        unsigned long long h[4] = {0, 0, 0, 0};
+        CU(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        for (int j = 0; j < 4; ++j) out[j] = (int64_t)h[j];
+    });
 }
 
 int es_dataset_destroy(es_dataset* ds) {

@@ -10,6 +10,7 @@
 #include <sstream>
 
 #include "eventscope/detect.hpp"
+#include "eventscope/eval.hpp"
 #include "eventscope/gmm.hpp"
 #include "eventscope_b200.h"
 
@@ -230,10 +231,9 @@ double calibrate_threshold(const GmmModel& model, const FeatureMatrix& X_train, 
     return calibrate_threshold_log(model, X_train, q, mode).first;
 }
 
-PipelineResult run_pipeline(const FeatureMatrix& X, const DetectorConfig& cfg, const FitOptions& opts,
-                            bool standardize) {
-    Dataset ds;
-    upload(X, ds);
+namespace {
+PipelineResult run_pipeline_on(Dataset& ds, const FeatureMatrix& X, const DetectorConfig& cfg, const FitOptions& opts,
+                               bool standardize) {
     const int d = X.dim, K = cfg.K;
     es_pipeline_cfg c{};
     c.K = K;
@@ -268,6 +268,108 @@ PipelineResult run_pipeline(const FeatureMatrix& X, const DetectorConfig& cfg, c
     for (int j = 0; j < d; ++j) r.standardization.emplace_back(mean[j], scale[j]);
     r.n_train = (std::int64_t)std::floor(cfg.train_window * (double)X.rows);
     return r;
+}
+}  // namespace
+
+PipelineResult run_pipeline(const FeatureMatrix& X, const DetectorConfig& cfg, const FitOptions& opts,
+                            bool standardize) {
+    Dataset ds;
+    upload(X, ds);
+    return run_pipeline_on(ds, X, cfg, opts, standardize);
+}
+
+// ------------------------------------------------------------------ eval-bench
+ConfusionMatrix confusion(const std::vector<std::uint8_t>& labels, const std::vector<std::uint8_t>& flags) {
+    if (labels.size() != flags.size()) throw Error::data("LengthMismatch", "labels and flags differ in length");
+    int64_t out[4] = {0, 0, 0, 0};
+    check(es_confusion(ctx(), labels.data(), flags.data(), (int64_t)labels.size(), out));
+    return ConfusionMatrix{out[0], out[1], out[2], out[3]};
+}
+
+EvalSummary metrics(const ConfusionMatrix& cm) {
+    const double n = (double)(cm.tp + cm.fp + cm.tn + cm.fn);
+    if (!(n > 0)) throw Error::data("EmptyMatrix", "confusion matrix has no events");
+    EvalSummary e;
+    e.cm = cm;
+    e.accuracy = (double)(cm.tp + cm.tn) / n;
+    e.precision = cm.tp + cm.fp ? (double)cm.tp / (double)(cm.tp + cm.fp) : 0.0;
+    e.recall = cm.tp + cm.fn ? (double)cm.tp / (double)(cm.tp + cm.fn) : 0.0;
+    e.f1 = e.precision + e.recall > 0.0 ? 2.0 * e.precision * e.recall / (e.precision + e.recall) : 0.0;
+    return e;
+}
+
+KMeansBaseline kmeans_baseline(const FeatureMatrix& X, int K, double q, std::uint64_t seed, double train_window,
+                               int max_iter) {
+    Dataset ds;
+    upload(X, ds);
+    KMeansBaseline r;
+    r.centroids.resize((size_t)std::max(K, 0) * X.dim);
+    r.flags.resize(X.rows);
+    r.scores.resize(X.rows);
+    int32_t it = 0;
+    check(es_kmeans_baseline(ctx(), ds.ds, K, q, train_window, seed, max_iter, r.centroids.data(), &r.threshold,
+                             r.flags.data(), r.scores.data(), &r.n_flagged, &it));
+    r.iterations = it;
+    return r;
+}
+
+std::vector<SweepCell> sensitivity_sweep(const FeatureMatrix& X, const std::vector<std::uint8_t>& labels,
+                                         const std::vector<int>& K_range, const std::vector<double>& q_range,
+                                         const std::vector<std::uint64_t>& seeds, const std::string& layer,
+                                         double train_window) {
+    if (K_range.empty() || q_range.empty() || seeds.empty())
+        throw Error::data("EmptyRange", "K_range, q_range and seeds must be nonempty");
+    if ((int64_t)labels.size() != X.rows) throw Error::data("LengthMismatch", "labels do not match the events");
+    Dataset ds;
+    upload(X, ds);  // one upload shared by every cell
+    std::vector<SweepCell> grid;
+    for (int K : K_range)
+        for (double q : q_range) {
+            SweepCell c;
+            c.layer = layer;
+            c.K = K;
+            c.q = q;
+            double acc[4] = {0, 0, 0, 0};
+            for (std::uint64_t sd : seeds) {
+                try {
+                    DetectorConfig cfg;
+                    cfg.K = K;
+                    cfg.quantile_q = q;
+                    cfg.train_window = train_window;
+                    FitOptions fo;
+                    fo.seed = sd;
+                    const PipelineResult pr = run_pipeline_on(ds, X, cfg, fo, true);
+                    const EvalSummary e = metrics(confusion(labels, pr.report.flags));
+                    acc[0] += e.accuracy;
+                    acc[1] += e.precision;
+                    acc[2] += e.recall;
+                    acc[3] += e.f1;
+                    ++c.seed_count;
+                } catch (const Error& e) {
+                    c.status = e.name();
+                }
+            }
+            if (c.seed_count) {
+                c.accuracy = acc[0] / c.seed_count;
+                c.precision = acc[1] / c.seed_count;
+                c.recall = acc[2] / c.seed_count;
+                c.f1 = acc[3] / c.seed_count;
+            } else {
+                c.accuracy = c.precision = c.recall = c.f1 = NAN;
+            }
+            grid.push_back(c);
+        }
+    return grid;
+}
+
+std::string sweep_csv(const std::vector<SweepCell>& grid) {
+    std::ostringstream o;
+    o.precision(17);
+    o << "layer,K,q,seed_count,accuracy,precision,recall,f1,status\n";
+    for (const SweepCell& c : grid)
+        o << c.layer << ',' << c.K << ',' << c.q << ',' << c.seed_count << ',' << c.accuracy << ',' << c.precision
+          << ',' << c.recall << ',' << c.f1 << ',' << c.status << '\n';
+    return o.str();
 }
 
 // ------------------------------------------------------------------ JSON

@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "eventscope/detect.hpp"
+#include "eventscope/eval.hpp"
 #include "eventscope/gmm.hpp"
 
 int main() {
@@ -45,6 +46,18 @@ int main() {
     PipelineResult pr = run_pipeline(Xi, DetectorConfig{std::nullopt, 0.01, 2, 0.5, DetectMode::Component}, FitOptions{});
     ok = ok && pr.report.flags.size() == (size_t)X.rows && pr.standardization.size() == (size_t)X.dim &&
          pr.n_train == X.rows / 2 && pr.report.delta > 0.0 && pr.report.model.K == 2;
+    // eval-bench: k-means baseline on the interleaved clusters, confusion / metrics
+    KMeansBaseline kb = kmeans_baseline(Xi, 2, 0.01, 5);
+    const int lo2 = kb.centroids[0] < kb.centroids[1] ? 0 : 1;
+    ok = ok && std::fabs(kb.centroids[lo2] + 5) < 0.2 && std::fabs(kb.centroids[1 - lo2] - 5) < 0.2 &&
+         kb.flags.size() == (size_t)Xi.rows && kb.iterations >= 1;
+    const ConfusionMatrix cm = confusion({1, 1, 0, 0}, {1, 0, 1, 0});
+    const EvalSummary es = metrics(cm);
+    ok = ok && cm.tp == 1 && cm.fp == 1 && cm.tn == 1 && cm.fn == 1 && std::fabs(es.f1 - 0.5) < 1e-15;
+    const std::vector<SweepCell> grid =
+        sensitivity_sweep(Xi, std::vector<std::uint8_t>(Xi.rows, 0), {2}, {0.01}, {0, 1});
+    ok = ok && grid.size() == 1 && grid[0].status == "ok" && grid[0].seed_count == 2 &&
+         sweep_csv(grid).rfind("layer,K,q,", 0) == 0;
     // JSON round trip (within 1e-15 per entry)
     GmmModel back = model_from_json(to_json(m));
     for (size_t i = 0; i < m.covariances.size(); ++i) ok = ok && back.covariances[i] == m.covariances[i];
