@@ -20,6 +20,7 @@
  *   es_run_pipeline          <- run_pipeline
  *   es_kmeans_baseline       <- kmeans_baseline
  *   es_confusion             <- confusion
+ *   es_events_extract        <- extract_features        SPEC.md:62-70 (+ validate_event :52-60)
  *
  * Conventions
  *  - Plain pointers and sizes only.  Parameters are host FP64 arrays, row-major:
@@ -216,6 +217,26 @@ int es_kmeans_baseline(es_ctx* ctx, es_dataset* ds, int32_t K, double q, double 
                        int32_t max_iter, double* centroids /* K*D, nullable */, double* threshold,
                        uint8_t* flags /* n_local, nullable */, double* scores /* n_local, nullable */,
                        int64_t* n_flagged, int32_t* iterations);
+/* Columnar events (SPEC.md:32-38 TraceEvent numeric fields; the attrs this build uses as
+ * columns, NaN = absent).  Layers: */
+enum { ES_LAYER_CUDA = 0, ES_LAYER_PYTHON = 1, ES_LAYER_TORCH = 2, ES_LAYER_NCCL = 3, ES_LAYER_GPU_SAMPLE = 4 };
+typedef struct es_event_columns {
+    const uint8_t* layer;        /* n, ES_LAYER_* */
+    const int64_t* ts_start;     /* n, ns since epoch, > 0 */
+    const int64_t* duration_ns;  /* n, >= 0 */
+    const double* message_bytes; /* n or NULL: Nccl attr, >= 0 */
+    const double* util_pct;      /* n or NULL: GpuSample attrs */
+    const double* mem_used_mb;
+    const double* temp_c;
+} es_event_columns;
+/* extract_features on the device: validates every event (first violation -> Data error
+ * RangeViolation / UnknownLayer / MissingField, its row in *bad_row), keeps `layer`'s
+ * events in order and writes the layer's default features (Cuda/Python/Torch:
+ * log10(duration_ns+1); Nccl: + log10(message_bytes+1); GpuSample: util, mem, temp) into a
+ * new dataset; event_index (n capacity, nullable) receives the source event of each row.
+ * EmptyLayer when no event has the layer. */
+int es_events_extract(es_ctx* ctx, const es_event_columns* cols, int64_t n, int32_t layer, es_dataset** out,
+                      int64_t* event_index, int64_t* bad_row);
 /* out = {tp, fp, tn, fn}, anomaly = positive class; labels / flags host or device. */
 int es_confusion(es_ctx* ctx, const uint8_t* labels, const uint8_t* flags, int64_t n, int64_t* out);
 

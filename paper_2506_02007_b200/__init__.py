@@ -654,3 +654,7 @@ def sensitivity_sweep(X, labels, K_range: Sequence[int], q_range: Sequence[float
             w.writeheader()
             w.writerows(rows)
     return rows
+
+
+from .events import (EventColumns, extract_features, from_records, read_columnar, read_trace_jsonl,  # noqa: E402
+                     write_columnar)

@@ -1635,4 +1635,75 @@ void launch_confusion(const uint8_t* labels, const uint8_t* flags, int64_t n, un
     ++ls.launches;
 }
 
+
+// ------------------------------------------------------------------ event features
+// (event-model extract_features, with validate_event's invariants,
+// SPEC.md:32-38,52-60).  Pass 1: keep_i = (layer_i == L); the first row violating an
+// invariant (min row index, then its field code) via atomicMin on (row << 8 | field).
+// Pass 2 (over the order-preserving compacted indices): the layer's default features,
+// Cuda/Python/Torch: log10(duration_ns + 1); Nccl: log10(duration_ns + 1),
+// log10(message_bytes + 1); GpuSample: util_pct, mem_used_mb, temp_c.
+__global__ void k_event_keep(const uint8_t* __restrict__ layer, const int64_t* __restrict__ ts,
+                             const int64_t* __restrict__ dur, const double* __restrict__ mb,
+                             const double* __restrict__ util, const double* __restrict__ mem,
+                             const double* __restrict__ temp, int64_t n, int L, uint8_t* __restrict__ keep,
+                             unsigned long long* __restrict__ bad) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int l = layer[i];
+        int f = 0;
+        // field code (1 layer, 2 ts_start, 3 duration_ns, 4 message_bytes, 5 util_pct,
+        // 6 mem_used_mb, 7 temp_c) | 0x10 when the attribute is absent (NULL column / NaN)
+        auto miss = [&](const double* col) { return !col || isnan(col[i]); };
+        if (l > 4) f = 1;
+        else if (!(ts[i] > 0)) f = 2;
+        else if (!(dur[i] >= 0)) f = 3;
+        else if (l == 3 && miss(mb)) f = 0x14;
+        else if (l == 3 && !(mb[i] >= 0.0)) f = 4;
+        else if (l == 4 && miss(util)) f = 0x15;
+        else if (l == 4 && !(util[i] >= 0.0 && util[i] <= 100.0)) f = 5;
+        else if (l == 4 && miss(mem)) f = 0x16;
+        else if (l == 4 && !(mem[i] >= 0.0)) f = 6;
+        else if (l == 4 && miss(temp)) f = 0x17;
+        else if (l == 4 && !(temp[i] > -50.0 && temp[i] < 150.0)) f = 7;
+        if (f) atomicMin(bad, ((unsigned long long)i << 8) | (unsigned long long)f);
+        keep[i] = (l == L) ? 1 : 0;
+    }
+}
+
+__global__ void k_event_features(const int64_t* __restrict__ idx, int64_t m, const int64_t* __restrict__ dur,
+                                 const double* __restrict__ mb, const double* __restrict__ util,
+                                 const double* __restrict__ mem, const double* __restrict__ temp, int L,
+                                 double* __restrict__ X, int64_t ld) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = idx[r];
+        if (L == 4) {
+            X[r] = util[i];
+            X[ld + r] = mem[i];
+            X[2 * ld + r] = temp[i];
+        } else {
+            X[r] = log10((double)dur[i] + 1.0);
+            if (L == 3) X[ld + r] = log10(mb[i] + 1.0);
+        }
+    }
+}
+
+void launch_event_keep(const uint8_t* layer, const int64_t* ts, const int64_t* dur, const double* mb,
+                       const double* util, const double* mem, const double* temp, int64_t n, int L, uint8_t* keep,
+                       unsigned long long* bad, int num_sms, cudaStream_t s, LaunchStats& ls) {
+    cudaMemsetAsync(bad, 0xFF, sizeof(unsigned long long), s);
+    if (n <= 0) return;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(8 * num_sms, (n + kBlock - 1) / kBlock));
+    k_event_keep<<<grid, kBlock, 0, s>>>(layer, ts, dur, mb, util, mem, temp, n, L, keep, bad);
+    ++ls.launches;
+}
+
+void launch_event_features(const int64_t* idx, int64_t m, const int64_t* dur, const double* mb, const double* util,
+                           const double* mem, const double* temp, int L, double* X, int64_t ld, int num_sms,
+                           cudaStream_t s, LaunchStats& ls) {
+    if (m <= 0) return;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(8 * num_sms, (m + kBlock - 1) / kBlock));
+    k_event_features<<<grid, kBlock, 0, s>>>(idx, m, dur, mb, util, mem, temp, L, X, ld);
+    ++ls.launches;
+}
+
 }  // namespace es

@@ -143,4 +143,12 @@ void launch_flag_gt(const double* score, int64_t n, double thr, uint8_t* flags, 
 void launch_confusion(const uint8_t* labels, const uint8_t* flags, int64_t n, unsigned long long* out, int num_sms,
                       cudaStream_t s, LaunchStats& ls);
 
+// event features (extract_features): validation + layer filter, then the layer's features
+void launch_event_keep(const uint8_t* layer, const int64_t* ts, const int64_t* dur, const double* mb,
+                       const double* util, const double* mem, const double* temp, int64_t n, int L, uint8_t* keep,
+                       unsigned long long* bad, int num_sms, cudaStream_t s, LaunchStats& ls);
+void launch_event_features(const int64_t* idx, int64_t m, const int64_t* dur, const double* mb, const double* util,
+                           const double* mem, const double* temp, int L, double* X, int64_t ld, int num_sms,
+                           cudaStream_t s, LaunchStats& ls);
+
 }  // namespace es

@@ -1279,6 +1279,91 @@ int es_confusion(es_ctx* c, const uint8_t* labels, const uint8_t* flags, int64_t
     });
 }
 
+// extract_features on the device from columnar events: validation of the
+// TraceEvent invariants (first violating row reported), the layer filter
+// (order-preserving compaction) and the layer's default features, straight into a
+// library-owned planar dataset.  Columns may be host or device arrays.
+int es_events_extract(es_ctx* c, const es_event_columns* cols, int64_t n, int32_t layer, es_dataset** out,
+                      int64_t* event_index, int64_t* bad_row) {
+    return guard([&] {
+        CU(cudaSetDevice(c->device));
+        if (bad_row) *bad_row = -1;
+        if (!cols || !out) fail(ES_ERR_DATA, "InvalidArgument", "null argument");
+        if (n < 0) fail(ES_ERR_DATA, "RangeViolation", "negative event count");
+        if (layer < 0 || layer > 4) fail(ES_ERR_DATA, "UnknownLayer", "layer must be 0..4");
+        if (n > 0 && (!cols->layer || !cols->ts_start || !cols->duration_ns))
+            fail(ES_ERR_DATA, "MissingField", "layer, ts_start and duration_ns columns are required");
+        const int D = layer == ES_LAYER_GPU_SAMPLE ? 3 : (layer == ES_LAYER_NCCL ? 2 : 1);
+        // device copies of host columns (8-byte aligned slices of one buffer)
+        const int64_t n8 = (n + 7) & ~int64_t(7);
+        std::vector<const void*> src = {cols->layer, cols->ts_start, cols->duration_ns, cols->message_bytes,
+                                        cols->util_pct, cols->mem_used_mb, cols->temp_c};
+        const size_t width[7] = {1, 8, 8, 8, 8, 8, 8};
+        size_t tot = 0;
+        for (int j = 0; j < 7; ++j) tot += (size_t)n8 * width[j];
+        unsigned char* buf = c->o1.as<unsigned char>(std::max<size_t>(tot, 8));
+        std::vector<const void*> dptr(7, nullptr);
+        size_t off = 0;
+        for (int j = 0; j < 7; ++j) {
+            if (src[j] && n > 0) {
+                if (is_device_ptr(src[j])) {
+                    dptr[j] = src[j];
+                } else {
+                    CU(cudaMemcpyAsync(buf + off, src[j], (size_t)n * width[j], cudaMemcpyHostToDevice, c->stream));
+                    dptr[j] = buf + off;
+                }
+            }
+            off += (size_t)n8 * width[j];
+        }
+        const auto* L = static_cast<const uint8_t*>(dptr[0]);
+        const auto* ts = static_cast<const int64_t*>(dptr[1]);
+        const auto* du = static_cast<const int64_t*>(dptr[2]);
+        const auto* mb = static_cast<const double*>(dptr[3]);
+        const auto* ut = static_cast<const double*>(dptr[4]);
+        const auto* me = static_cast<const double*>(dptr[5]);
+        const auto* te = static_cast<const double*>(dptr[6]);
+        uint8_t* keep = c->o2.as<uint8_t>(std::max<int64_t>(n, 1));
+        unsigned long long* bad = c->hist.as<unsigned long long>(256);
+        launch_event_keep(L, ts, du, mb, ut, me, te, n, layer, keep, bad, c->num_sms, c->stream, c->ls);
+        c->check_launch();
+        unsigned long long hb = ~0ull;
+        CU(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        if (hb != ~0ull) {
+            static const char* names[8] = {"", "layer", "ts_start", "duration_ns", "message_bytes", "util_pct",
+                                           "mem_used_mb", "temp_c"};
+            const int64_t row = (int64_t)(hb >> 8);
+            const int f = (int)(hb & 0xFF);
+            if (bad_row) *bad_row = row;
+            fail(ES_ERR_DATA, f == 1 ? "UnknownLayer" : (f & 0x10) ? "MissingField" : "RangeViolation",
+                 std::string(names[f & 0xF]) + ((f & 0x10) ? " missing" : " out of range") + " at event " +
+                     std::to_string(row));
+        }
+        const int64_t nc = (n + 4095) / 4096;
+        int64_t* cnt = c->o3.as<int64_t>(std::max<int64_t>(nc, 1) + 8);
+        int64_t* idx = c->o4.as<int64_t>(std::max<int64_t>(n, 1));
+        int64_t* dm = cnt + std::max<int64_t>(nc, 1);
+        launch_compact(keep, n, 0, cnt, idx, dm, c->stream, c->ls);
+        c->check_launch();
+        int64_t m = 0;
+        CU(cudaMemcpyAsync(&m, dm, 8, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        if (m == 0) fail(ES_ERR_DATA, "EmptyLayer", "no events of the requested layer");
+        auto ds = std::make_unique<es_dataset>();
+        ds->ctx = c;
+        ds->n_local = m;
+        ds->D = D;
+        ds->ld = plane_ld(m);
+        CU(cudaMalloc(&ds->X, (size_t)ds->ld * D * 8));
+        launch_event_features(idx, m, du, mb, ut, me, te, layer, ds->X, ds->ld, c->num_sms, c->stream, c->ls);
+        c->check_launch();
+        if (event_index) CU(cudaMemcpyAsync(event_index, idx, (size_t)m * 8, cudaMemcpyDefault, c->stream));
+        c->sync();
+        finish_dataset(c, ds.get());
+        *out = ds.release();
+    });
+}
+
 int es_dataset_destroy(es_dataset* ds) {
     return guard([&] { delete ds; });
 }

@@ -11,6 +11,7 @@
 
 #include "eventscope/detect.hpp"
 #include "eventscope/eval.hpp"
+#include "eventscope/events.hpp"
 #include "eventscope/gmm.hpp"
 #include "eventscope_b200.h"
 
@@ -276,6 +277,41 @@ PipelineResult run_pipeline(const FeatureMatrix& X, const DetectorConfig& cfg, c
     Dataset ds;
     upload(X, ds);
     return run_pipeline_on(ds, X, cfg, opts, standardize);
+}
+
+// ------------------------------------------------------------------ event features
+FeatureMatrix extract_features(const EventColumns& e, Layer layer) {
+    const int64_t n = (int64_t)e.layer.size();
+    if ((int64_t)e.ts_start.size() != n || (int64_t)e.duration_ns.size() != n)
+        throw Error::data("LengthMismatch", "event columns differ in length");
+    auto opt = [&](const std::vector<double>& v) -> const double* {
+        if (v.empty()) return nullptr;
+        if ((int64_t)v.size() != n) throw Error::data("LengthMismatch", "event columns differ in length");
+        return v.data();
+    };
+    es_event_columns c{e.layer.data(), e.ts_start.data(), e.duration_ns.data(), opt(e.message_bytes),
+                       opt(e.util_pct), opt(e.mem_used_mb), opt(e.temp_c)};
+    Dataset ds;
+    std::vector<int64_t> idx(std::max<int64_t>(n, 1));
+    int64_t bad = -1;
+    check(es_events_extract(ctx(), &c, n, (int32_t)layer, &ds.ds, idx.data(), &bad));
+    int64_t nl = 0, ng = 0, off = 0;
+    int32_t D = 0;
+    check(es_dataset_info(ds.ds, &nl, &ng, &off, &D));
+    FeatureMatrix X;
+    X.rows = nl;
+    X.dim = D;
+    X.data.resize((size_t)nl * D);
+    check(es_dataset_read_rows(ds.ds, 0, nl, X.data.data()));
+    idx.resize(nl);
+    X.event_index = std::move(idx);
+    if (layer == Layer::GpuSample)
+        X.feature_names = {"util_pct", "mem_used_mb", "temp_c"};
+    else if (layer == Layer::Nccl)
+        X.feature_names = {"log10_duration_ns", "log10_message_bytes"};
+    else
+        X.feature_names = {"log10_duration_ns"};
+    return X;
 }
 
 // ------------------------------------------------------------------ eval-bench

@@ -8,6 +8,7 @@
 
 #include "eventscope/detect.hpp"
 #include "eventscope/eval.hpp"
+#include "eventscope/events.hpp"
 #include "eventscope/gmm.hpp"
 
 int main() {
@@ -58,6 +59,14 @@ int main() {
         sensitivity_sweep(Xi, std::vector<std::uint8_t>(Xi.rows, 0), {2}, {0.01}, {0, 1});
     ok = ok && grid.size() == 1 && grid[0].status == "ok" && grid[0].seed_count == 2 &&
          sweep_csv(grid).rfind("layer,K,q,", 0) == 0;
+    // extract_features on the device: Nccl duration 999, 9 bytes -> [3, 1]
+    EventColumns ec;
+    ec.layer = {3, 0};
+    ec.ts_start = {10, 20};
+    ec.duration_ns = {999, 99};
+    ec.message_bytes = {9.0, NAN};
+    const FeatureMatrix F = extract_features(ec, Layer::Nccl);
+    ok = ok && F.rows == 1 && F.dim == 2 && F.data[0] == 3.0 && F.data[1] == 1.0 && F.event_index[0] == 0;
     // JSON round trip (within 1e-15 per entry)
     GmmModel back = model_from_json(to_json(m));
     for (size_t i = 0; i < m.covariances.size(); ++i) ok = ok && back.covariances[i] == m.covariances[i];
