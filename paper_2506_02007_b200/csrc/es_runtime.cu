@@ -171,8 +171,33 @@ struct es_ctx {
     ncclComm_t comm = nullptr;
     es_exchange ex{};
     cudaStream_t stream = nullptr;
+    cudaStream_t cstream = nullptr;          // host->device copies of dataset_create (overlap the transposes)
+    cudaEvent_t evc[2] = {nullptr, nullptr}, evt[2] = {nullptr, nullptr};
     int num_sms = 148;
     LaunchStats ls;
+    DevBuf stage2;  // second staging buffer of dataset_create
+    // the planes of the last destroyed dataset, kept for the next dataset_create of a
+    // similar size (an 8.6 GB cudaMalloc / cudaFree pair per fit-on-fresh-data call is
+    // ~20 ms plus a device synchronisation)
+    void* plane_cache = nullptr;
+    size_t plane_cache_bytes = 0;
+    double* take_planes(size_t bytes) {
+        if (plane_cache && plane_cache_bytes >= bytes && plane_cache_bytes <= 2 * bytes) {
+            void* p = plane_cache;
+            plane_cache = nullptr;
+            plane_cache_bytes = 0;
+            return static_cast<double*>(p);
+        }
+        void* p = nullptr;
+        CU(cudaMalloc(&p, bytes));
+        return static_cast<double*>(p);
+    }
+    void give_planes(void* p, size_t bytes) {
+        cudaStreamSynchronize(stream);
+        if (plane_cache) cudaFree(plane_cache);
+        plane_cache = p;
+        plane_cache_bytes = bytes;
+    }
     DevBuf partial, stats_local, stats_all, model, model_backup, status, scratch, scratch2, scratch3, out_scratch,
         hist, xbuf, o1, o2, o3, o4, o5, kpp, center;
     std::vector<double> center_host;  // host copy of `center` (scoring kernels' FP64 centre)
@@ -262,10 +287,17 @@ struct es_dataset {
     double* X = nullptr;
     CUtensorMap xmap{};      // TMA descriptor over X (D <= 16), see make_event_tmap
     bool has_xmap = false;
-    ~es_dataset() {
-        if (X) cudaFree(X);
-    }
+    bool owned_by_cache = false;  // planes from es_ctx::take_planes (returned there on destroy)
+    ~es_dataset();
 };
+
+es_dataset::~es_dataset() {
+    if (!X) return;
+    if (owned_by_cache && ctx)
+        ctx->give_planes(X, (size_t)ld * D * 8);
+    else
+        cudaFree(X);
+}
 
 struct es_em_state {
     es_ctx* ctx = nullptr;
@@ -817,7 +849,13 @@ static void ctx_common(es_ctx* c, int device) {
     c->device = device;
     CU(cudaSetDevice(device));
     CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+        CU(cudaEventCreateWithFlags(&c->evc[i], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&c->evt[i], cudaEventDisableTiming));
+    }
     CU(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+
     CU(cudaMallocHost(&c->h_status, sizeof(IterStatus)));
 }
 
@@ -881,6 +919,13 @@ int es_ctx_destroy(es_ctx* c) {
         if (c->h_status) cudaFreeHost(c->h_status);
         if (c->ev0) cudaEventDestroy(c->ev0);
         if (c->ev1) cudaEventDestroy(c->ev1);
+        cudaStreamSynchronize(c->cstream);
+        if (c->plane_cache) cudaFree(c->plane_cache);
+        for (int i = 0; i < 2; ++i) {
+            if (c->evc[i]) cudaEventDestroy(c->evc[i]);
+            if (c->evt[i]) cudaEventDestroy(c->evt[i]);
+        }
+        cudaStreamDestroy(c->cstream);
         cudaStreamDestroy(c->stream);
         delete c;
     });
@@ -946,7 +991,8 @@ int es_dataset_create(es_ctx* c, const double* X, int64_t n_local, int32_t D, in
         ds->n_local = n_local;
         ds->D = D;
         ds->ld = plane_ld(std::max<int64_t>(n_local, 1));
-        CU(cudaMalloc(&ds->X, (size_t)ds->ld * D * 8));
+        ds->X = c->take_planes((size_t)ds->ld * D * 8);
+        ds->owned_by_cache = true;
         if (n_local > 0) {
             if (!X) fail(ES_ERR_DATA, "InvalidInput", "null matrix");
             const bool dev = is_device_ptr(X);
@@ -970,13 +1016,24 @@ int es_dataset_create(es_ctx* c, const double* X, int64_t n_local, int32_t D, in
                 CU(cudaMemcpy2DAsync(ds->X, ds->ld * 8, X, col_stride * 8, n_local * 8, D, cudaMemcpyDefault,
                                      c->stream));
             } else {
+                // 64 MB chunks, two staging buffers: the copy of chunk i + 1 (copy stream)
+                // overlaps the row -> plane transpose of chunk i (compute stream)
                 const int64_t chunk = std::max<int64_t>(1, (64ll << 20) / (8 * D));
-                double* stage = c->scratch3.as<double>((size_t)std::min(chunk, n_local) * D);
-                for (int64_t r0 = 0; r0 < n_local; r0 += chunk) {
+                double* stage[2] = {c->scratch3.as<double>((size_t)std::min(chunk, n_local) * D),
+                                    c->stage2.as<double>((size_t)std::min(chunk, n_local) * D)};
+                CU(cudaEventRecord(c->evt[0], c->stream));  // the allocation is ordered before the copies
+                CU(cudaStreamWaitEvent(c->cstream, c->evt[0], 0));
+                int64_t ci = 0;
+                for (int64_t r0 = 0; r0 < n_local; r0 += chunk, ++ci) {
+                    const int b = (int)(ci & 1);
                     const int64_t nr = std::min(chunk, n_local - r0);
-                    CU(cudaMemcpyAsync(stage, X + r0 * D, (size_t)nr * D * 8, cudaMemcpyDefault, c->stream));
-                    launch_rows_to_planar(stage, nr, D, ds->X, ds->ld, r0, c->stream, c->ls);
+                    if (ci >= 2) CU(cudaStreamWaitEvent(c->cstream, c->evt[b], 0));  // buffer b transposed
+                    CU(cudaMemcpyAsync(stage[b], X + r0 * D, (size_t)nr * D * 8, cudaMemcpyDefault, c->cstream));
+                    CU(cudaEventRecord(c->evc[b], c->cstream));
+                    CU(cudaStreamWaitEvent(c->stream, c->evc[b], 0));
+                    launch_rows_to_planar(stage[b], nr, D, ds->X, ds->ld, r0, c->stream, c->ls);
                     c->check_launch();
+                    CU(cudaEventRecord(c->evt[b], c->stream));
                 }
             }
             c->sync();
