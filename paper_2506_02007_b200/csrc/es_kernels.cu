@@ -996,14 +996,17 @@ void launch_score(const double* X, int64_t n, int64_t ld, int D, int K, const do
 // (q = sum_a (x_a - mu_ka)^2 / sigma2_ka) and accumulates its 2D+1 statistics
 // about c_k = mu_k(old) in FP64 registers.  Statistics use the canonical
 // packed layout with only the diagonal of s2 populated (finalize in diag mode).
+constexpr int DTILE = kBlock;  // events per staged tile of k_em_diag (one per thread)
+
 template <int DM>
-__global__ void __launch_bounds__(kBlock) k_em_diag(const double* __restrict__ X, int64_t n, int64_t ld, int D, int K,
+__global__ void __launch_bounds__(kBlock, DM <= 16 ? 2 : 1) k_em_diag(const double* __restrict__ X, int64_t n, int64_t ld, int D, int K,
                                                    const double* __restrict__ model, double* __restrict__ partial) {
     extern __shared__ __align__(16) double sm[];
     const int MS = DM + 1;
     double* sMu = sm;                 // K * MS
     double* sP = sMu + K * MS;        // K * MS  (precisions 1/sigma^2)
     double* sC = sP + K * MS;         // 2K: logpi, lognorm
+    double* sX = sC + 2 * K;          // [DM][DTILE] staged event tile (coalesced loads)
     const int TS = next_pow2(K);
     const int EPW = 32 / TS;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1031,24 +1034,53 @@ __global__ void __launch_bounds__(kBlock) k_em_diag(const double* __restrict__ X
 #pragma unroll
     for (int j = 0; j < NA; ++j) acc[j] = 0.0;
     double ll_acc = 0.0;
-    for (int64_t it = 0;; ++it) {
-        const int64_t wbase = ((it * gridDim.x + blockIdx.x) * 8 + warp) * EPW;
-        if (wbase >= n) break;
-        const int64_t i = wbase + slot;
+    // tiles of DTILE events: staged into shared memory with coalesced loads (thread t loads
+    // event t of the tile, every feature), the next tile prefetched into registers while
+    // this one is evaluated; inside a tile, warp w / slot s take events (r * 8 + w) * EPW + s
+    constexpr bool PF = DM <= 16;
+    double pf[PF ? DM : 1];
+    const int64_t ntl = (n + DTILE - 1) / DTILE;
+    auto fetch = [&](int64_t tl_idx, double* dst) {
+        const int64_t i = tl_idx * DTILE + threadIdx.x;
+#pragma unroll
+        for (int j = 0; j < DM; ++j) dst[j] = (i < n && j < D) ? __ldg(X + (int64_t)j * ld + i) : 0.0;
+    };
+    if (PF && blockIdx.x < ntl) fetch(blockIdx.x, pf);
+    for (int64_t tt = blockIdx.x; tt < ntl; tt += gridDim.x) {
+        __syncthreads();  // the previous tile is consumed
+        if (PF) {
+#pragma unroll
+            for (int j = 0; j < DM; ++j) sX[j * DTILE + threadIdx.x] = pf[j];
+        } else {
+            double tmp[DM];
+            fetch(tt, tmp);
+#pragma unroll
+            for (int j = 0; j < DM; ++j) sX[j * DTILE + threadIdx.x] = tmp[j];
+        }
+        __syncthreads();
+        if (PF && tt + gridDim.x < ntl) fetch(tt + gridDim.x, pf);
+      for (int rr = 0; rr < DTILE / (8 * EPW); ++rr) {
+        const int le = (rr * 8 + warp) * EPW + slot;
+        const int64_t i = tt * DTILE + le;
         const bool valid = i < n;
         double d[DM];
         double q = 0.0;
 #pragma unroll
         for (int j = 0; j < DM; ++j) {
-            const double x = (valid && j < D) ? __ldg(X + (int64_t)j * ld + i) : 0.0;
+            const double x = sX[j * DTILE + le];
             d[j] = (j < D) ? x - muk[j] : 0.0;
             q = fma(d[j] * d[j], pk[j], q);
         }
         const double ln = lognorm - 0.5 * q;
         const double w = kact ? logpi + ln : -INFINITY;
-        const TeamLse r = team_lse<1>(w, kact ? ln : -INFINITY, k, TS);
-        const double g = (valid && kact) ? exp(w - r.ll) : 0.0;
-        if (valid && tl == 0) ll_acc += r.ll;
+        // team log-sum-exp; gamma = exp(w - m) / sum (one FP64 exp per lane)
+        double m = w;
+        for (int off = 1; off < TS; off <<= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+        const double e = kact ? exp(w - m) : 0.0;
+        double ssum = e;
+        for (int off = 1; off < TS; off <<= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, off);
+        const double g = (valid && kact) ? e / ssum : 0.0;
+        if (valid && tl == 0) ll_acc += m + log(ssum);
         acc[0] += g;
 #pragma unroll
         for (int j = 0; j < DM; ++j) {
@@ -1056,6 +1088,7 @@ __global__ void __launch_bounds__(kBlock) k_em_diag(const double* __restrict__ X
             acc[1 + j] += gd;
             acc[1 + DM + j] = fma(gd, d[j], acc[1 + DM + j]);
         }
+      }
     }
     // slots within the warp, then warps in order (fixed-order reduction)
 #pragma unroll
@@ -1104,7 +1137,7 @@ void launch_em_diag(const double* X, int64_t n, int64_t ld, int D, int K, const 
     *nblk = grid;
     const int TS = next_pow2(K);
     auto smem_for = [&](int DM) {
-        const size_t a = (size_t)(2 * K * (DM + 1) + 2 * K) * sizeof(double);
+        const size_t a = (size_t)(2 * K * (DM + 1) + 2 * K + DM * DTILE) * sizeof(double);
         const size_t b = (size_t)8 * TS * (1 + 2 * DM) * sizeof(double);
         return a > b ? a : b;
     };
