@@ -42,10 +42,14 @@ def main():
         d, ld = es.calibrate_threshold(m, ds, 0.01, n_train=n // 2, return_log=True)
         r = es.detect(m, ds, log_delta=ld)
         mk = es.fit_em(ds, 4, init="kmeans++", tol=0.0, max_iter=3, seed=5)
+        kb = es.kmeans_baseline(ds, 4, q=0.02, seed=3)
+        pr = es.run_pipeline(ds, 4, quantile_q=0.02, seed=1, max_iter=10)
         np.savez(out + f".{rank}.npz", w=m.weights, mu=m.means, cov=m.covariances,
                  per=m.fit_report.per_iteration_log_likelihoods, final=m.fit_report.final_log_likelihood,
                  delta=d, ld=ld, idx=r.anomaly_indices, nflag=r.n_flagged, off=ds.row_offset,
-                 kmu=mk.means, kw=mk.weights)
+                 kmu=mk.means, kw=mk.weights, kbc=kb.centroids, kbt=kb.threshold, kbn=kb.n_flagged,
+                 kbf=kb.flags, kbi=kb.iterations, pmu=pr.model.means, pmean=pr.mean, pscale=pr.scale,
+                 pdelta=pr.report.delta, pn=pr.report.n_flagged, pf=pr.report.flags)
     dist.destroy_process_group()
 
 

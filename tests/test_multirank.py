@@ -81,3 +81,20 @@ def test_two_ranks_match_single_rank(tmp_path):
     assert len(np.setxor1d(both, r.anomaly_indices)) <= 1e-4 * n  # models differ at 1e-8: threshold band only
     mk = es.fit_em(ds, 4, init="kmeans++", tol=0.0, max_iter=3, seed=5)
     assert np.allclose(z0["kmu"], mk.means, rtol=1e-5, atol=1e-6)
+    # k-means baseline: rank-ordered Lloyd sums -> the same centroids / threshold on both ranks
+    kb = es.kmeans_baseline(ds, 4, q=0.02, seed=3)
+    for key in ("kbc", "kbt", "kbn", "kbi"):
+        assert np.array_equal(z0[key], z1[key]), key
+    assert int(z0["kbi"]) == kb.iterations
+    np.testing.assert_allclose(z0["kbc"], kb.centroids, rtol=1e-10, atol=1e-12)
+    assert abs(float(z0["kbt"]) - kb.threshold) <= 1e-10 * kb.threshold
+    both = np.concatenate([z0["kbf"], z1["kbf"]])
+    assert np.sum(both != kb.flags) <= 2 and abs(int(z0["kbn"]) - kb.n_flagged) <= 2
+    # run_pipeline over the shards (the train split is rank 0's rows)
+    pr = es.run_pipeline(ds, 4, quantile_q=0.02, seed=1, max_iter=10)
+    for key in ("pmu", "pmean", "pscale", "pdelta", "pn"):
+        assert np.array_equal(z0[key], z1[key]), key
+    np.testing.assert_allclose(z0["pmean"], pr.mean, rtol=1e-12)
+    np.testing.assert_allclose(z0["pmu"], pr.model.means, rtol=1e-5, atol=1e-6)
+    pf = np.concatenate([z0["pf"], z1["pf"]])
+    assert np.sum(pf != pr.report.flags) <= 1e-4 * n
