@@ -982,10 +982,16 @@ void launch_score(const double* X, int64_t n, int64_t ld, int D, int K, const do
                   double* blocksum, int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls) {
     const int grid = score_grid(D, K, num_sms);
     *nblk = grid;
+    // the team kernels keep every component's W in shared memory: beyond the opt-in limit
+    // (D = 32 with K > 26) the generic kernel reads the model from global memory
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (K <= 32 && D <= 4) run_score_team<4>(X, n, ld, D, K, model, o, blocksum, grid, s);
     else if (K <= 32 && D <= 8) run_score_team<8>(X, n, ld, D, K, model, o, blocksum, grid, s);
     else if (K <= 32 && D <= 16) run_score_team<16>(X, n, ld, D, K, model, o, blocksum, grid, s);
-    else if (K <= 32 && D <= 32) run_score_team<32>(X, n, ld, D, K, model, o, blocksum, grid, s);
+    else if (K <= 32 && D <= 32 && team_smem<32, 1>(K, false) <= (size_t)optin)
+        run_score_team<32>(X, n, ld, D, K, model, o, blocksum, grid, s);
     else k_score_generic<<<grid, kBlock, 0, s>>>(X, n, ld, D, K, model, o, blocksum);
     ++ls.launches;
 }
