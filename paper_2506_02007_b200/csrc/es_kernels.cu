@@ -1234,6 +1234,11 @@ __global__ void k_derive(double* model, int D, int K, IterStatus* st) {
 }
 
 void launch_derive(double* model, int D, int K, IterStatus* st, cudaStream_t s, LaunchStats& ls) {
+    static bool attr = false;  // 3 D^2 doubles: 96 KB at D = 64 (opt-in above 48 KB)
+    if (!attr) {
+        allow_max_smem(k_derive);
+        attr = true;
+    }
     k_derive<<<K, 128, 3 * D * D * sizeof(double), s>>>(model, D, K, st);
     ++ls.launches;
 }

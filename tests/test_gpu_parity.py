@@ -109,7 +109,8 @@ def _fit_both(es, oracle, ds, X, K, iters, init="random", seed=7):
 
 
 @pytest.mark.parametrize("D,K,n,iters", [(8, 4, 1 << 20, 100), (16, 8, 1 << 17, 12), (3, 5, 100_003, 40),
-                                         (20, 3, 30_011, 10), (2, 40, 20_000, 8), (32, 32, 40_000, 5)])
+                                         (20, 3, 30_011, 10), (2, 40, 20_000, 8), (32, 32, 40_000, 5),
+                                         (48, 3, 20_000, 4), (64, 2, 10_007, 3)])
 def test_fit_score_detect_parity(es, oracle, prec, D, K, n, iters):
     ds, X = syn(es, oracle, n, D, min(K, 8))
     model, (pi, mu, cov, rep) = _fit_both(es, oracle, ds, X, K, iters)
