@@ -720,6 +720,38 @@ bool mixed_em(es_ctx* c, const es_em_state* st) {
     return c->precision == 0 && em_fast_supported(st->D, st->K) && st->min_nk >= kMixedMinNk;
 }
 
+// logL of the current model from one fused tcgen05 E+M pass (statistics discarded): the
+// same FP32 log-sum-exp per event as every per-iteration logL, half the cost of the
+// refined scorer; used for final_log_likelihood on the mixed path.
+bool em_logl_pass(es_em_state* st, double* out) {
+    es_ctx* c = st->ctx;
+    es_dataset* ds = st->ds;
+    const int K = st->K, D = st->D;
+    if (is_diag(st) || !mixed_em(c, st) || !em_mma_enabled() || !ds->has_xmap) return false;
+    const int NE1 = stat_total(D, K);
+    double* dmodel = c->model.as<double>(mstride(K, D));
+    double* loc = c->stats_local.as<double>(NE1);
+    if (ds->n_local > 0) {
+        int nblk = 0;
+        double* part = c->partial.as<double>((size_t)std::max(em_grid(D, K, c->num_sms), c->num_sms) * NE1);
+        const int np = st->min_nk >= kOnePassMinNk ? 1 : 2;
+        launch_em_mma(&ds->xmap, ds->n_local, D, K, dmodel, st->dcenter.as<double>(D), st->mean.data(), st->xs,
+                      st->f32conv, np, part, c->num_sms, &nblk, c->stream, c->ls);
+        launch_reduce_blocks(part, nblk, NE1, loc, c->stream, c->ls);
+        c->check_launch();
+    } else {
+        CU(cudaMemsetAsync(loc, 0, NE1 * 8, c->stream));
+    }
+    double ll = 0.0;
+    CU(cudaMemcpyAsync(&ll, loc + (NE1 - 1), 8, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    const std::vector<double> all = c->allgather_host(&ll, 1);  // rank-ordered sum
+    double tot = 0.0;
+    for (double v : all) tot += v;
+    *out = tot;
+    return true;
+}
+
 // One EM iteration; returns true when the loop must stop.
 bool em_iterate(es_em_state* st) {
     es_ctx* c = st->ctx;
@@ -1493,7 +1525,8 @@ int es_gmm_em_end(es_em_state* st, es_gmm_params* out, es_fit_report* rep, doubl
         const int K = st->K, D = st->D;
         double* dmodel = c->model.as<double>(mstride(K, D));
         double final_ll = st->last;
-        if (!st->converged) final_ll = run_score(c, st->ds, dmodel, K, ScoreOut{}, st->dcenter.as<double>(D), st->mean.data(), st->xs);
+        if (!st->converged && !em_logl_pass(st, &final_ll))
+            final_ll = run_score(c, st->ds, dmodel, K, ScoreOut{}, st->dcenter.as<double>(D), st->mean.data(), st->xs);
         if (out) {
             if (out->K != K || out->D != D) fail(ES_ERR_DATA, "DimensionMismatch", "output params shape");
             ModelView mv{K, D, dmodel};
