@@ -5,8 +5,8 @@
 //   converter WG  thread = event: coalesced loads of the FP64 planes (one tile of
 //                 prefetch in registers), x^ = (x - c) xs -> an FP32 row (for the
 //                 records) and the fp16 hi + lo K-major UMMA operand.
-//   MMA warp      E:  U = W' x^ + b'  as 4 kind::f16 dispatches (x_hi W_hi,
-//                     x_hi W_lo, x_lo W_hi, 1 * [b_hi b_lo]) -> TMEM, M = N = 128;
+//   MMA warp      E:  U = b' + W' x^  as 4 kind::f16 dispatches (1 * fp32(b') first, then x_hi W_hi,
+//                     x_hi W_lo, x_lo W_hi) -> TMEM, M = N = 128;
 //                 M:  Gram of the tile's per-event records over its 128 events
 //                     (8 K-steps of 16 events), M = 128 rows (k, a).
 //   epilogue WG   thread = event = TMEM lane: squared norms of U, log-sum-exp,
@@ -85,7 +85,7 @@ struct Smem {
     unsigned char rech[NWG][RECH];                      // hi records (per warpgroup)
     unsigned char recl[NPASS == 2 ? NWG : 1][NPASS == 2 ? RECL : 16];  // 2 x lo records
     unsigned char bw[2][OPB];                           // W' hi / lo
-    unsigned char bb[OPB];                              // b' hi, lo in K columns 0, 1
+    unsigned char bb[OPB];                              // fp32(b') as three fp16 parts in K columns 0-2
     double c[DM];
     double shift[NWG][KMAX * DM];                       // record centre - starting centre (FP64, exact)
     double dl[NWG][KMAX * DM], s1x[NWG][KMAX * DM];     // recentring exchange
@@ -156,8 +156,8 @@ __global__ void __launch_bounds__(nthr(NWG), 1) k_em_mma(const __grid_constant__
     tc_fence_after();
     const uint32_t tmem = S.tmem;
     auto tile_of = [&](int64_t j) { return (int64_t)blockIdx.x + j * gridDim.x; };
-    if (warp < 4) {  // ones in K columns 0, 1 of every row: the bias dispatch's A operand
-        const uint32_t one[8] = {0x3C003C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    if (warp < 4) {  // ones in K columns 0-2 of every row: the bias dispatch's A operand
+        const uint32_t one[8] = {0x3C003C00u, 0x00003C00u, 0u, 0u, 0u, 0u, 0u, 0u};  // K columns 0, 1, 2
         tmem_st8(tmem + ((uint32_t)(32 * warp) << 16) + TONE, one);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
@@ -567,10 +567,10 @@ __global__ void __launch_bounds__(nthr(NWG), 1) k_em_mma(const __grid_constant__
                     TRACE(1, je);
                     tc_fence_after();
                     const uint32_t tah = tmem + TA0 + 16 * w, tal = tah + 8;
-                    mma_f16_ta(tmem, tah, dbh, kIdescE, 0u);
+                    mma_f16_ta(tmem, tmem + TONE, dbb, kIdescE, 0u);  // fp32(b') exactly, first
+                    mma_f16_ta(tmem, tah, dbh, kIdescE, 1u);
                     mma_f16_ta(tmem, tah, dbl, kIdescE, 1u);
                     mma_f16_ta(tmem, tal, dbh, kIdescE, 1u);
-                    mma_f16_ta(tmem, tmem + TONE, dbb, kIdescE, 1u);
                     commit(&S.edone[w]);
                     TRACE(9, je);
                     ++je;

@@ -203,9 +203,17 @@ __device__ inline void stage_estep(const ModelView& mv, int K, int D, const doub
         const __half wl = __double2half(w - (double)__half2float(wh));
         *reinterpret_cast<__half*>(bw0 + kmaj(row, f)) = wh;
         *reinterpret_cast<__half*>(bw1 + kmaj(row, f)) = wl;
-        const __half bh = __double2half(b);
-        const __half bl = __double2half(b - (double)__half2float(bh));
-        *reinterpret_cast<__half*>(bb + kmaj(row, f)) = f == 0 ? bh : (f == 1 ? bl : __half(0.f));
+        // b' rounded once to FP32 and split exactly into three fp16 parts (11 + 11 + 2 bits):
+        // the bias dispatch, issued first, then leaves exactly fp32(b') in the accumulator,
+        // and the whitening dispatches add onto it, so the running sums stay of the size of
+        // U instead of |W' x^| ~ |b'| (FP32 truncation ~1 ulp of the running sum per dispatch)
+        const float b32 = (float)b;
+        const __half bh = __float2half_rn(b32);
+        const float r1 = b32 - __half2float(bh);
+        const __half bm = __float2half_rn(r1);
+        const __half bl = __float2half_rn(r1 - __half2float(bm));
+        *reinterpret_cast<__half*>(bb + kmaj(row, f)) =
+            f == 0 ? bh : (f == 1 ? bm : (f == 2 ? bl : __half(0.f)));
     }
 }
 

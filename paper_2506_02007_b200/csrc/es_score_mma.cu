@@ -107,8 +107,8 @@ __global__ void __launch_bounds__(NTHR, 1) k_score_mma(const __grid_constant__ C
     tc_fence_after();
     const uint32_t tmem = S.tmem;
     auto tile_of = [&](int64_t j) { return (int64_t)blockIdx.x + j * gridDim.x; };
-    if (warp < 4) {  // ones in K columns 0, 1 of every row: the bias dispatch's A operand
-        const uint32_t one[8] = {0x3C003C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    if (warp < 4) {  // ones in K columns 0-2 of every row: the bias dispatch's A operand
+        const uint32_t one[8] = {0x3C003C00u, 0x00003C00u, 0u, 0u, 0u, 0u, 0u, 0u};  // K columns 0, 1, 2
         tmem_st8(tmem + ((uint32_t)(32 * warp) << 16) + TONE, one);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
@@ -348,10 +348,10 @@ __global__ void __launch_bounds__(NTHR, 1) k_score_mma(const __grid_constant__ C
                 if (je >= 1) mbar_wait_sleep(su32(&S.efree), (uint32_t)((je - 1) & 1));
                 tc_fence_after();
                 const uint32_t tah = tmem + TA0 + 16 * w, tal = tah + 8;
-                mma_f16_ta(tmem, tah, dbh, kIdescE, 0u);
+                mma_f16_ta(tmem, tmem + TONE, dbb, kIdescE, 0u);  // fp32(b') exactly, first
+                mma_f16_ta(tmem, tah, dbh, kIdescE, 1u);
                 mma_f16_ta(tmem, tah, dbl, kIdescE, 1u);
                 mma_f16_ta(tmem, tal, dbh, kIdescE, 1u);
-                mma_f16_ta(tmem, tmem + TONE, dbb, kIdescE, 1u);
                 commit(&S.edone[w]);
             }
         }
