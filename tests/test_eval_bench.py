@@ -131,3 +131,23 @@ def test_sensitivity_sweep(es, tmp_path):
     rows = es.sensitivity_sweep(X[:40], y[:40], [2, 3000], [1e-3, 1e-2], seeds=[0, 1])
     assert [(c["K"], c["q"]) for c in rows] == [(2, 1e-3), (2, 1e-2), (3000, 1e-3), (3000, 1e-2)]
     assert rows[0]["status"] == "ok" and rows[2]["status"] != "ok" and rows[2]["seed_count"] == 0
+
+
+@pytest.mark.gpu
+def test_empty_inputs(es):
+    """Empty event matrices: scoring / detect are no-ops, fits and calibration raise the
+    SPEC's data errors."""
+    X0 = np.empty((0, 4))
+    rng = np.random.default_rng(0)
+    m = es.GmmModel(np.array([0.5, 0.5]), rng.normal(size=(2, 4)), np.tile(np.eye(4), (2, 1, 1)))
+    assert es.score(m, X0, ll=np.empty(0)) == 0.0
+    r = es.detect(m, X0, log_delta=-5.0)
+    assert r.n_flagged == 0 and len(r.flags) == 0
+    with pytest.raises(es.EventscopeError):
+        es.fit_em(X0, 2)
+    with pytest.raises(es.EventscopeError):
+        es.calibrate_threshold(m, X0, 0.01, n_train=0)
+    with pytest.raises(es.EventscopeError):
+        es.kmeans_baseline(X0, 2)
+    with pytest.raises(es.EventscopeError):
+        es.run_pipeline(X0, 2)
