@@ -30,7 +30,10 @@ namespace {
 
 using namespace mma;
 
-constexpr int NWG = 3;             // epilogue warpgroups (tiles j = w mod NWG)
+#ifndef ES_SCORE_NWG  // 3: 7.3 ms per 2^26-event pass; 2 (168 registers): 8.0 ms
+#define ES_SCORE_NWG 3
+#endif
+constexpr int NWG = ES_SCORE_NWG;  // epilogue warpgroups (tiles j = w mod NWG)
 constexpr int NTHR = 128 * NWG + 64;  // + TMA warp + MMA warp
 constexpr int WTMA = 4 * NWG, WMMA = 4 * NWG + 1;
 constexpr int XS = 2 * NWG;        // FP64 tile stages: each WG holds its tile and the next one
