@@ -915,7 +915,10 @@ int es_ctx_create_nccl(int device, int rank, int world, const unsigned char id[1
         ctx_common(c.get(), device);
         c->rank = rank;
         c->world = world;
-        if (world > 1) {
+        // ES_FORCE_NCCL=1: a one-rank NCCL communicator too (tests the NCCL exchange path
+        // on a single GPU)
+        const char* fe = std::getenv("ES_FORCE_NCCL");
+        if (world > 1 || (fe && fe[0] == '1')) {
             ncclUniqueId u;
             std::memcpy(&u, id, 128);
             NC(nccl().CommInitRank(&c->comm, world, u, rank));

@@ -98,3 +98,32 @@ def test_two_ranks_match_single_rank(tmp_path):
     np.testing.assert_allclose(z0["pmu"], pr.model.means, rtol=1e-5, atol=1e-6)
     pf = np.concatenate([z0["pf"], z1["pf"]])
     assert np.sum(pf != pr.report.flags) <= 1e-4 * n
+
+
+@pytest.mark.gpu
+def test_nccl_exchange_one_rank(monkeypatch):
+    """The NCCL exchange path (stat all-gather, histogram all-reduce, k-means++ / Lloyd host
+    sums) on a one-rank NCCL communicator reproduces the single-context results bitwise."""
+    import ctypes as C
+
+    import paper_2506_02007_b200 as es
+    monkeypatch.setenv("ES_FORCE_NCCL", "1")
+    lib = es.load_library()
+    h = C.c_void_p()
+    idb = (C.c_ubyte * 128).from_buffer_copy(es.Context.nccl_unique_id())
+    assert lib.es_ctx_create_nccl(0, 0, 1, idb, C.byref(h)) == 0
+    nc = es.Context.__new__(es.Context)
+    nc._lib, nc._keep, nc.handle, nc.device, nc.rank, nc.world = lib, None, h, 0, 0, 1
+    nc.set_precision("mixed")
+    ref = es.Context(0)
+    out = []
+    for ctx in (nc, ref):
+        ds = es.Dataset.generate(42, 100_003, 16, 8, ctx=ctx)
+        m = es.fit_em(ds, 8, init="kmeans++", tol=0.0, max_iter=4, seed=3, ctx=ctx)
+        d, ld = es.calibrate_threshold(m, ds, 0.01, n_train=50_000, return_log=True)
+        kb = es.kmeans_baseline(ds, 4, q=0.02, seed=1)
+        out.append((m.means, m.covariances, m.fit_report.per_iteration_log_likelihoods, ld, kb.centroids,
+                    kb.threshold))
+        ds.close()
+    for a, b in zip(*out):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
