@@ -687,6 +687,43 @@ int eso_kmeans_baseline(const double* X, int64_t N, int D, int K, double q, doub
     return kOk;
 }
 
+// Lloyd's iterations from given centroids (the kmeans_baseline inner loop), for pinning the
+// restatement against an external implementation (tests/test_eval_bench.py vs sklearn).
+int eso_lloyd(const double* X, int64_t N, int D, int K, double* centroids, int max_iter, int* iterations) {
+    std::vector<int> asg(N, -1);
+    int it = 0;
+    while (it < max_iter) {
+        int64_t changed = 0;
+        std::vector<double> sum((size_t)K * D, 0.0), cnt(K, 0.0);
+        for (int64_t i = 0; i < N; ++i) {
+            double b = INFINITY;
+            int bk = 0;
+            for (int k = 0; k < K; ++k) {
+                double d2 = 0.0;
+                for (int a = 0; a < D; ++a) {
+                    const double e = X[(size_t)i * D + a] - centroids[(size_t)k * D + a];
+                    d2 = std::fma(e, e, d2);
+                }
+                if (d2 < b) {
+                    b = d2;
+                    bk = k;
+                }
+            }
+            if (asg[i] != bk) ++changed;
+            asg[i] = bk;
+            cnt[bk] += 1.0;
+            for (int a = 0; a < D; ++a) sum[(size_t)bk * D + a] += X[(size_t)i * D + a];
+        }
+        ++it;
+        for (int k = 0; k < K; ++k)
+            if (cnt[k] > 0.0)
+                for (int a = 0; a < D; ++a) centroids[(size_t)k * D + a] = sum[(size_t)k * D + a] / cnt[k];
+        if (changed == 0) break;
+    }
+    *iterations = it;
+    return kOk;
+}
+
 // confusion: out = {tp, fp, tn, fn}, anomaly = positive class
 int eso_confusion(const uint8_t* labels, const uint8_t* flags, int64_t n, int64_t* out) {
     out[0] = out[1] = out[2] = out[3] = 0;

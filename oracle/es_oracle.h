@@ -92,6 +92,7 @@ int eso_detect(const double* X, int64_t N, int D, const double* pi, const double
 int eso_kmeans_baseline(const double* X, int64_t N, int D, int K, double q, double train_window, uint64_t seed,
                         int max_iter, double* centroids, double* threshold, uint8_t* flags, double* scores,
                         int64_t* n_flagged, int* iterations, int nthreads);
+int eso_lloyd(const double* X, int64_t N, int D, int K, double* centroids, int max_iter, int* iterations);
 int eso_confusion(const uint8_t* labels, const uint8_t* flags, int64_t n, int64_t* out);
 int eso_calibrate(const double* X, int64_t n_train, int D, const double* pi,
                   const double* mu, const double* cov, int K, double q, int mode,

@@ -192,6 +192,16 @@ def kmeans_baseline(X, K, q=0.01, train_window=0.5, seed=0, max_iter=100, nthrea
     return cen, thr.value, flags, scores, nf.value, it.value
 
 
+def lloyd(X, centroids, max_iter=300):
+    """Lloyd's iterations from given centroids (the kmeans_baseline inner loop)."""
+    X = np.ascontiguousarray(X, np.float64)
+    cen = np.array(centroids, np.float64, order="C", copy=True)
+    it = C.c_int()
+    _check(lib().eso_lloyd(_p(X), C.c_int64(X.shape[0]), X.shape[1], cen.shape[0], _p(cen), max_iter,
+                           C.byref(it)))
+    return cen, it.value
+
+
 def confusion(labels, flags):
     """SPEC.md:431-437: (tp, fp, tn, fn), anomaly = positive class."""
     lab = np.ascontiguousarray(labels, np.uint8)

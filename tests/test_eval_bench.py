@@ -151,3 +151,15 @@ def test_empty_inputs(es):
         es.kmeans_baseline(X0, 2)
     with pytest.raises(es.EventscopeError):
         es.run_pipeline(X0, 2)
+
+
+def test_lloyd_oracle_matches_sklearn(oracle):
+    """The oracle's Lloyd loop (nearest centroid, ties -> lowest k, stop when no assignment
+    changes) against scikit-learn's KMeans(algorithm="lloyd", tol=0) from the same start."""
+    from sklearn.cluster import KMeans
+    X, _ = blobs(4000, 5, 6, seed=21, spread=4.0)
+    rng = np.random.default_rng(3)
+    init = X[rng.choice(len(X), 6, replace=False)]
+    cen, it = oracle.lloyd(X, init, max_iter=300)
+    km = KMeans(n_clusters=6, init=init, n_init=1, max_iter=300, tol=0.0, algorithm="lloyd").fit(X)
+    np.testing.assert_allclose(cen, km.cluster_centers_, rtol=1e-12, atol=1e-12)
