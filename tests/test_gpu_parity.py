@@ -329,3 +329,14 @@ def test_run_pipeline_errors_and_fixed_delta(es, oracle):
     of, _, obl, _ = oracle.detect(X2, r.model.weights, r.model.means, r.model.covariances, np.log(1e-3))
     mism = np.nonzero(r.report.flags != of)[0]
     assert np.all(np.abs(obl[mism] - np.log(1e-3)) < BAND)
+
+
+@pytest.mark.parametrize("n", [1 << 16, 1 << 24])
+def test_em_monotone_on_device(es, prec, n):
+    """SPEC.md:299,312 (acceptance #1): the logL trajectory is nondecreasing within 1e-8
+    (relative), through the default mixed path and the strict FP64 path, small and large N."""
+    ctx = es.Context(0, precision=prec)
+    ds = es.Dataset.generate(11, n, 16, 8, ctx=ctx)
+    m = es.fit_em(ds, 8, init="random", tol=0.0, max_iter=12, seed=3, ctx=ctx)
+    per = m.fit_report.per_iteration_log_likelihoods
+    assert np.all(np.diff(per) >= -1e-8 * np.abs(per[1:])), np.diff(per)
