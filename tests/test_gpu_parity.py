@@ -340,3 +340,25 @@ def test_em_monotone_on_device(es, prec, n):
     m = es.fit_em(ds, 8, init="random", tol=0.0, max_iter=12, seed=3, ctx=ctx)
     per = m.fit_report.per_iteration_log_likelihoods
     assert np.all(np.diff(per) >= -1e-8 * np.abs(per[1:])), np.diff(per)
+
+
+def test_detect_properties_full_size(es):
+    """At 2^24 events (size-independent properties): anomaly sets are nested in delta
+    (SPEC.md:388, acceptance #7) and the calibrated threshold flags the q-quantile of the
+    train split: #{train: log p < log delta} = floor(h) + 1 or so."""
+    n, q = 1 << 24, 0.01
+    ds = es.Dataset.generate(5, n, 16, 8)
+    m = es.fit_em(ds, 8, init="random", tol=0.0, max_iter=5, seed=1)
+    d, ld = es.calibrate_threshold(m, ds, q, n_train=n // 2, return_log=True)
+    r = es.detect(m, ds, log_delta=ld, indices=False)
+    bl = r.log_density
+    ntr = int(np.sum(bl[: n // 2] < ld))
+    h = (n // 2 - 1) * q
+    assert int(np.floor(h)) <= ntr <= int(np.floor(h)) + 1
+    prev = None
+    for lds in np.linspace(ld - 5.0, ld + 5.0, 10):
+        f = es.detect(m, ds, log_delta=float(lds), indices=False).flags.astype(bool)
+        assert np.array_equal(f, bl < lds)
+        if prev is not None:
+            assert np.all(f[prev])  # A(delta_i) subset of A(delta_i+1)
+        prev = f
