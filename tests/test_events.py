@@ -142,3 +142,25 @@ def test_columnar_to_pipeline(es, tmp_path):
     b = es.run_pipeline(X, 3, quantile_q=0.02, seed=1)
     assert np.array_equal(a.report.flags, b.report.flags)
     np.testing.assert_allclose(a.model.means, b.model.means, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.gpu
+def test_extract_permutation_and_standardization(es):
+    """extract_features is order preserving (permuting events permutes rows)
+    and the train-split z-scoring of run_pipeline gives columns with |mean| < 1e-9 and stddev
+    within 1e-9 of 1 (FeatureMatrix invariant); x * sigma + m recovers the raw
+    features within 1e-9."""
+    recs = random_records(6000, seed=12)
+    cols = ev.from_records(recs)
+    ds, idx = es.extract_features(cols, "Nccl")
+    X = ds.read_rows()
+    perm = np.random.default_rng(1).permutation(len(recs))
+    ds2, idx2 = es.extract_features(ev.from_records([recs[i] for i in perm]), "Nccl")
+    X2 = ds2.read_rows()
+    pos = {e: r for r, e in enumerate(idx)}
+    assert np.array_equal(X2, X[[pos[perm[e]] for e in idx2]])
+    r = es.run_pipeline(ds, 3, quantile_q=0.02, seed=0)
+    ntr = r.n_train
+    Z = (X[:ntr] - r.mean) / r.scale
+    assert np.all(np.abs(Z.mean(0)) < 1e-9) and np.all(np.abs(Z.std(0) - 1.0) < 1e-9)
+    assert np.allclose(Z * r.scale + r.mean, X[:ntr], rtol=0, atol=1e-9)
