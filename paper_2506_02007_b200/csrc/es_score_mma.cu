@@ -50,9 +50,8 @@ struct SmemS {
     double wred[4 * NWG][2];
     unsigned char bw[2][OPB];
     unsigned char bb[OPB];
-    uint8_t cev[NWG][KMAX * TM + KMAX];      // compacted candidates (component-major): event
-    uint8_t ccomp[NWG][KMAX * TM + KMAX];    //                                       component
-    int wcnt[NWG][KMAX * 4], woff[NWG][KMAX * 4], ncand[NWG];
+    uint8_t cev[NWG][4 * (KMAX * 32 + KMAX)];    // compacted candidates per warp (component-major): event
+    uint8_t ccomp[NWG][4 * (KMAX * 32 + KMAX)];  //                                                component
     float cst[KMAX], lnf[KMAX], hq[KMAX], tk[KMAX];
     uint64_t xfull[XS], xfree[XS], aeready[NWG], edone[NWG], efree;
     uint32_t tmem;
@@ -95,7 +94,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_score_mma(const __grid_constant__ C
     if (t == 0) {
         for (int i = 0; i < XS; ++i) {
             mbar_init(&S.xfull[i], 1);
-            mbar_init(&S.xfree[i], 1);
+            mbar_init(&S.xfree[i], 4);  // one arrival per warp of the warpgroup that refines the tile
         }
         for (int i = 0; i < NWG; ++i) {
             mbar_init(&S.aeready[i], 1);
@@ -208,45 +207,35 @@ __global__ void __launch_bounds__(NTHR, 1) k_score_mma(const __grid_constant__ C
                         (ln[k] == bl && fabsf(bl - ldf) <= 1e-3f * (1.f + fabsf(ldf)));
                 if (valid && k < K && (c || ovf)) cand |= 1u << k;
             }
-            // component-major compaction inside the warpgroup (fixed order: component, warp, lane)
-            unsigned kb[KMAX];
+            // component-major compaction inside the warp (fixed order: component, lane); each
+            // component segment padded to an even length (two events of one component per item).
+            // Warp-local: no warpgroup barrier, each warp refines its own 32 events.
+            uint8_t* cev = S.cev[w] + q * (KMAX * 32 + KMAX);
+            uint8_t* ccomp = S.ccomp[w] + q * (KMAX * 32 + KMAX);
+            int nc = 0;
 #pragma unroll
             for (int k = 0; k < KMAX; ++k) {
-                kb[k] = __ballot_sync(0xffffffffu, (cand >> k) & 1u);
-                if (lane == 0) S.wcnt[w][k * 4 + q] = __popc(kb[k]);
-            }
-            named_sync(1 + NWG + w, 128);
-            if (p == 0) {
-                int a2 = 0;
-                for (int k = 0; k < KMAX; ++k) {
-                    for (int wv = 0; wv < 4; ++wv) {
-                        S.woff[w][k * 4 + wv] = a2;
-                        a2 += S.wcnt[w][k * 4 + wv];
-                    }
-                    if (a2 & 1) {  // even segments: two events of one component per thread
-                        S.cev[w][a2] = 0xFFu;
-                        S.ccomp[w][a2] = (uint8_t)k;
-                        ++a2;
-                    }
-                }
-                S.ncand[w] = a2;
-            }
-            named_sync(1 + NWG + w, 128);
-#pragma unroll
-            for (int k = 0; k < KMAX; ++k) {
+                const unsigned kb = __ballot_sync(0xffffffffu, (cand >> k) & 1u);
                 if ((cand >> k) & 1u) {
-                    const int pos = S.woff[w][k * 4 + q] + __popc(kb[k] & lt_mask);
-                    S.cev[w][pos] = (uint8_t)p;
-                    S.ccomp[w][pos] = (uint8_t)k;
+                    const int pos = nc + __popc(kb & lt_mask);
+                    cev[pos] = (uint8_t)p;
+                    ccomp[pos] = (uint8_t)k;
+                }
+                nc += __popc(kb);
+                if (nc & 1) {
+                    if (lane == 0) {
+                        cev[nc] = 0xFFu;
+                        ccomp[nc] = (uint8_t)k;
+                    }
+                    ++nc;
                 }
             }
-            named_sync(1 + NWG + w, 128);
-            // FP64 refinement, two events of one component per thread (each W row load serves both)
-            const int nc = S.ncand[w];
+            __syncwarp();
+            // FP64 refinement, two events of one component per lane (each W row load serves both)
             double* lnv = S.lnv[w];
-            for (int pidx = 2 * p; pidx < nc; pidx += 2 * TM) {
-                const int k = S.ccomp[w][pidx];
-                const int e0 = S.cev[w][pidx], e1r = S.cev[w][pidx + 1];
+            for (int pidx = 2 * lane; pidx < nc; pidx += 64) {
+                const int k = ccomp[pidx];
+                const int e0 = cev[pidx], e1r = cev[pidx + 1];
                 const int e1 = e1r == 0xFF ? e0 : e1r;
                 const double* WTk = S.W64 + k * W64S;  // column f of W_k at WTk[f * DM + r]
                 const double* mk = S.mu64 + k * (DM + 2);
@@ -276,8 +265,8 @@ __global__ void __launch_bounds__(NTHR, 1) k_score_mma(const __grid_constant__ C
                 lnv[k * TM + e0] = S.ln64[k] - 0.5 * q0;
                 if (e1r != 0xFF) lnv[k * TM + e1] = S.ln64[k] - 0.5 * q1;
             }
-            named_sync(1 + NWG + w, 128);
-            if (p == 0) arrive(&S.xfree[s]);  // the FP64 tile is no longer needed
+            __syncwarp();
+            if (lane == 0) arrive(&S.xfree[s]);  // this warp no longer reads the FP64 tile
             double mm = -INFINITY, bb = -INFINITY;
             int am = 0, ab = 0;
             double w64[KMAX];
