@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_score_mma(const __grid_constant__ C
             mbar_init(&S.xfree[i], 4);  // one arrival per warp of the warpgroup that refines the tile
         }
         for (int i = 0; i < NWG; ++i) {
-            mbar_init(&S.aeready[i], 1);
+            mbar_init(&S.aeready[i], 4);
             mbar_init(&S.edone[i], 1);
         }
         mbar_init(&S.efree, 4);
@@ -155,8 +155,8 @@ __global__ void __launch_bounds__(NTHR, 1) k_score_mma(const __grid_constant__ C
             tmem_st8(tmem + lq + TA0 + 16 * w + 8, lw);
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
-            named_sync(1 + w, 128);
-            if (p == 0) arrive(&S.aeready[w]);
+            __syncwarp();
+            if (lane == 0) arrive(&S.aeready[w]);  // per warp: its 32 events are staged
             return !(vmax <= 16384.f);
         };
         bool ovf = w < J ? convert(w) : false, ovf_next = false;
