@@ -120,44 +120,65 @@ def max_over_ranks(v, world):
     return float(t.item())
 
 
-def cpu_baseline_sample(nthreads=None, iters=2, n_sample=1 << 19):
-    """Oracle (C++ FP64, OpenMP, all host cores) on a bounded sample of the
-    same workload: `iters` EM iterations on n_sample SYN-v1 rows; the per-event
-    rate is scaled to N=2^26 (time is linear in N)."""
+def cpu_em_setup(cores, X=None):
+    """The bench workload on the host for the CPU oracle: the full N=2^26 SYN-v1 matrix (the
+    same rows the device generator writes) and the same Random init (seed 7)."""
+    from oracle import oracle
+    if X is None:
+        model = oracle.syn_model(SEED, D, K)
+        X, _, _ = oracle.syn_rows(SEED, D, K, model, 0, N_GLOBAL, nthreads=cores)
+    pi, mu, cov, reg = oracle.random_init(X, K, 7)
+    return X, pi, mu, cov, reg
+
+
+def cpu_baseline_sample(X=None, nthreads=None):
+    """cpu_baseline of our arm: ONE EM iteration of the CPU oracle (C++ FP64, OpenMP, all host
+    cores) on the full N=2^26 matrix — the same workload as a bench step, no extrapolation.
+    X: the host copy of the bench matrix (row-major, already read back for e2e) or None."""
     from oracle import oracle
     cores = nthreads or os.cpu_count()
-    model = oracle.syn_model(SEED, D, K)
-    X, _, _ = oracle.syn_rows(SEED, D, K, model, 0, n_sample, nthreads=cores)
-    pi0, mu0, cov0, reg = oracle.random_init(X, K, 7)
+    X, pi, mu, cov, reg = cpu_em_setup(cores, X)
     t0 = time.perf_counter()
-    oracle.fit_em(X, K, init_params=(pi0, mu0, cov0), tol=0.0, max_iter=iters, reg=reg, nthreads=cores)
+    oracle.em_step(X, pi, mu, cov, reg, nthreads=cores)
     dt = time.perf_counter() - t0
-    # fit_em with tol=0 runs `iters` E+M passes plus one final E pass
-    per_iter = dt / (iters + 0.5) * (N_GLOBAL / n_sample)
-    return {"value": 1.0 / per_iter, "unit": "iters/s", "cores": cores, "kind": "port",
-            "sample": f"{iters} EM iterations (+final E pass) of the CPU oracle on {n_sample} of the {N_GLOBAL} "
-                      f"SYN-v1 rows, {cores} OpenMP threads, scaled linearly to N={N_GLOBAL}"}
+    return {"value": 1.0 / dt, "unit": "iters/s", "cores": cores, "kind": "port",
+            "sample": f"1 EM iteration (E-step + two-pass M-step, oracle eso_em_step) of the CPU oracle on the "
+                      f"full {N_GLOBAL}x{D} SYN-v1 matrix from the bench's Random init, {cores} OpenMP threads"}
 
 
 def run_reference(args):
+    """Reference arm: the CPU oracle port (the reference ships no buildable implementation,
+    DESIGN.md section 7) on the same config - W warm-up + K timed EM iterations over the full
+    N=2^26 matrix, each step one eso_em_step (E-step + literal two-pass M-step)."""
     rank, world, _ = dist_setup(args.gpus)
     if rank != 0:
         return
+    from oracle import oracle
     cores = os.cpu_count()
+    t0 = time.perf_counter()
+    X, pi, mu, cov, reg = cpu_em_setup(cores)
+    setup_s = time.perf_counter() - t0
     for _ in range(args.warmup):
-        pass
-    vals = []
-    for _ in range(max(1, args.steps)):
-        vals.append(cpu_baseline_sample(cores, iters=1, n_sample=1 << 18)["value"])
-    v = statistics.median(vals)
+        oracle.em_step(X, pi, mu, cov, reg, nthreads=cores)
+    t0 = time.perf_counter()
+    lls = []
+    for _ in range(args.steps):
+        lls.append(oracle.em_step(X, pi, mu, cov, reg, nthreads=cores)[0])
+    dt = time.perf_counter() - t0
+    v = args.steps / dt
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / v, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (SYN-v1, seed 42)",
-            "config": {"workload": WORKLOAD, "N": N_GLOBAL, "D": D, "K": K, "covariance": "full"},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (SYN-v1 seed 42, generated on the host by the oracle)",
+            "config": {"workload": WORKLOAD, "N": N_GLOBAL, "D": D, "K": K, "covariance": "full",
+                       "init": "random seed 7"},
             "cpu_baseline": {"value": v, "unit": "iters/s", "cores": cores, "kind": "port",
-                             "sample": "per step: 1 EM iteration (+final E pass) of the CPU oracle on 2^18 SYN-v1 "
-                                       "rows, all host threads, scaled linearly to N=2^26"},
-            "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                             "sample": f"every step: 1 EM iteration (oracle eso_em_step: E-step + two-pass "
+                                       f"M-step) on the full {N_GLOBAL}x{D} matrix, {cores} OpenMP threads, "
+                                       f"after {args.warmup} untimed warm-up iterations; host generation + "
+                                       f"init {setup_s:.1f} s untimed"},
+            "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "last_log_likelihood": lls[-1] if lls else None}
     print(json.dumps(line))
 
 
@@ -241,6 +262,7 @@ def run_ours(args):
     # host (pinned) event matrix -> es_dataset_create (H2D) -> EM iterations
     # -> parameters back to the host, all inside the timed region.
     e2e = None
+    hostX = None
     if not args.no_e2e:
         hostX = torch.empty((ds.n_local, D), dtype=torch.float64, pin_memory=True)
         ds.read_rows(out=hostX)
@@ -263,7 +285,6 @@ def run_ours(args):
                "note": f"per call: H2D of the {n_global}x{D} f64 matrix + data stats + Random init + {e2e_iters} "
                        f"EM iterations + final logL + params D2H; steps = EM iterations",
                "final_log_likelihood": m2.fit_report.final_log_likelihood}
-        del hostX
 
     if rank != 0:
         return
@@ -312,8 +333,8 @@ def run_ours(args):
         "clocks": clk.summary(),
         "e2e": e2e,
     }
-    if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline_sample()
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline_sample(hostX.numpy() if hostX is not None else None)
     print(json.dumps(line))
 
 

@@ -137,6 +137,12 @@ int es_dataset_create(es_ctx* ctx, const double* X, int64_t n_local, int32_t D, 
  * this rank receives global rows [r*n/G, (r+1)*n/G). */
 int es_dataset_generate(es_ctx* ctx, uint64_t seed, int64_t n_global, int32_t D, int32_t K_true,
                         es_dataset** out);
+/* Rows [row0, row0 + n_global) of the same SYN-v1 stream (a slice of a larger
+ * generated matrix, e.g. 2^26 rows at offset 2^29 of the 2^30-event c4 stream);
+ * this rank receives [row0 + r*n/G, row0 + (r+1)*n/G); row indices of the
+ * dataset are relative to row0. */
+int es_dataset_generate_range(es_ctx* ctx, uint64_t seed, int64_t row0, int64_t n_global, int32_t D,
+                              int32_t K_true, es_dataset** out);
 int es_dataset_destroy(es_dataset* ds);
 int es_dataset_info(es_dataset* ds, int64_t* n_local, int64_t* n_global, int64_t* row_offset, int32_t* D);
 /* Copies local rows [row0,row0+n) back out, row-major (tests / inspection). */

@@ -70,12 +70,16 @@ struct SplitMix64 {
 
 // ------------------------------------------------------ dense helpers ----
 // Lower Cholesky factor of a D x D SPD matrix (row-major). false if not PD.
+// "Not PD" (SingularCovariance) is numerical: a pivot at or below
+// D * 2^-46 of its diagonal entry (condition number beyond ~1e13 / D) counts as
+// singular, so that an exactly rank-deficient covariance is rejected whatever
+// the sign of the rounding noise in its pivots.
 bool cholesky(const double* A, int D, double* L) {
     std::fill(L, L + (size_t)D * D, 0.0);
     for (int j = 0; j < D; ++j) {
         double s = A[(size_t)j * D + j];
         for (int p = 0; p < j; ++p) s -= L[(size_t)j * D + p] * L[(size_t)j * D + p];
-        if (!(s > 0.0) || !std::isfinite(s)) return false;
+        if (!(s > std::ldexp((double)D, -46) * A[(size_t)j * D + j]) || !std::isfinite(s)) return false;
         double ljj = std::sqrt(s);
         L[(size_t)j * D + j] = ljj;
         for (int i = j + 1; i < D; ++i) {
@@ -363,6 +367,115 @@ int eso_random_init(const double* X, int64_t N, int D, int K, uint64_t seed, dou
     return kOk;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Work buffers of one EM iteration (gamma N x K and the chunk partials).
+struct EmWork {
+    std::vector<double> gamma, part_ll, part_nk, part_s1, part_s2;
+    void size(int64_t N, int D, int K) {
+        const int64_t C = nchunks(N);
+        gamma.resize((size_t)N * K);
+        part_ll.resize(C);
+        part_nk.resize((size_t)C * K);
+        part_s1.resize((size_t)C * K * D);
+        part_s2.resize((size_t)C * K * D * D);
+    }
+};
+
+// E-step: gamma (when kept) and logL = sum_i ll_i(theta), rows in
+// chunks, chunk partials summed in chunk order.
+int em_estep(const double* X, int64_t N, int D, int K, const double* pi, const double* mu, const double* cov,
+             EmWork& w, bool keep_gamma, double& logL) {
+    Factored f;
+    if (int s = factor(pi, mu, cov, K, D, f)) return s;
+    const int64_t C = nchunks(N);
+#pragma omp parallel
+    {
+        std::vector<double> z(D), wk(K);
+#pragma omp for schedule(static)
+        for (int64_t c = 0; c < C; ++c) {
+            double s = 0.0;
+            for (int64_t i = c * kChunk; i < std::min(N, (c + 1) * kChunk); ++i) {
+                RowScore r = score_row(f, X + (size_t)i * D, wk.data(), z.data());
+                s += r.ll;
+                if (keep_gamma)
+                    for (int k = 0; k < K; ++k) w.gamma[(size_t)i * K + k] = std::exp(wk[k] - r.ll);
+            }
+            w.part_ll[c] = s;
+        }
+    }
+    logL = 0.0;
+    for (int64_t c = 0; c < C; ++c) logL += w.part_ll[c];
+    return kOk;
+}
+
+// M-step, literal two-pass form of SPEC.md:294 (mean first, then the covariance about the
+// NEW mean); Nk receives sum_i gamma_ik.  Collapse handling is the caller's.
+void em_mstep(const double* X, int64_t N, int D, int K, double reg, bool diag, double* pi, double* mu, double* cov,
+              EmWork& w, std::vector<double>& Nk) {
+    const int64_t C = nchunks(N);
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < C; ++c) {
+        double* nk = &w.part_nk[(size_t)c * K];
+        double* s1 = &w.part_s1[(size_t)c * K * D];
+        std::fill(nk, nk + K, 0.0);
+        std::fill(s1, s1 + (size_t)K * D, 0.0);
+        for (int64_t i = c * kChunk; i < std::min(N, (c + 1) * kChunk); ++i)
+            for (int k = 0; k < K; ++k) {
+                double g = w.gamma[(size_t)i * K + k];
+                nk[k] += g;
+                for (int d = 0; d < D; ++d) s1[(size_t)k * D + d] += g * X[(size_t)i * D + d];
+            }
+    }
+    Nk.assign(K, 0.0);
+    for (int64_t c = 0; c < C; ++c)
+        for (int k = 0; k < K; ++k) Nk[k] += w.part_nk[(size_t)c * K + k];
+    for (int k = 0; k < K; ++k) {
+        for (int d = 0; d < D; ++d) {
+            double s = 0.0;
+            for (int64_t c = 0; c < C; ++c) s += w.part_s1[(size_t)c * K * D + (size_t)k * D + d];
+            mu[(size_t)k * D + d] = Nk[k] > 0 ? s / Nk[k] : mu[(size_t)k * D + d];
+        }
+        pi[k] = Nk[k] / (double)N;
+    }
+#pragma omp parallel
+    {
+        std::vector<double> y(D);
+#pragma omp for schedule(static)
+        for (int64_t c = 0; c < C; ++c) {
+            double* s2 = &w.part_s2[(size_t)c * K * D * D];
+            std::fill(s2, s2 + (size_t)K * D * D, 0.0);
+            for (int64_t i = c * kChunk; i < std::min(N, (c + 1) * kChunk); ++i)
+                for (int k = 0; k < K; ++k) {
+                    double g = w.gamma[(size_t)i * K + k];
+                    for (int d = 0; d < D; ++d) y[d] = X[(size_t)i * D + d] - mu[(size_t)k * D + d];
+                    for (int a = 0; a < D; ++a)
+                        for (int b = a; b < (diag ? a + 1 : D); ++b)
+                            s2[(size_t)k * D * D + (size_t)a * D + b] += g * y[a] * y[b];
+                }
+        }
+    }
+    for (int k = 0; k < K; ++k) {
+        double* ck = cov + (size_t)k * D * D;
+        for (int a = 0; a < D; ++a)
+            for (int b = a; b < D; ++b) {
+                double s = 0.0;
+                for (int64_t c = 0; c < C; ++c)
+                    s += w.part_s2[(size_t)c * K * D * D + (size_t)k * D * D + (size_t)a * D + b];
+                double v = Nk[k] > 0 ? s / Nk[k] : 0.0;
+                if (diag && a != b) v = 0.0;
+                ck[(size_t)a * D + b] = v + (a == b ? reg : 0.0);
+                ck[(size_t)b * D + a] = ck[(size_t)a * D + b];
+            }
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
 int eso_fit_em(const double* X, int64_t N, int D, int K, const eso_fit_opts* opts, const double* pi_init,
                const double* mu_init, const double* cov_init, double* pi, double* mu, double* cov,
                eso_fit_report* rep, double* per_iter) {
@@ -401,42 +514,18 @@ int eso_fit_em(const double* X, int64_t N, int D, int K, const eso_fit_opts* opt
         }
     }
 
-    const int64_t C = nchunks(N);
-    std::vector<double> gamma((size_t)N * K);
-    std::vector<double> part_ll(C), part_nk((size_t)C * K), part_s1((size_t)C * K * D);
-    std::vector<double> part_s2((size_t)C * K * D * D);
+    EmWork w;
+    w.size(N, D, K);
+    std::vector<double> Nk;
     int collapses = 0;
     int iterations = 0;
     bool converged = false;
     int nrec = 0;
     double prev = 0.0, cur = 0.0;
 
-    auto estep = [&](double& logL, bool keep_gamma) -> int {
-        Factored f;
-        if (int s = factor(pi, mu, cov, K, D, f)) return s;
-#pragma omp parallel
-        {
-            std::vector<double> z(D), w(K);
-#pragma omp for schedule(static)
-            for (int64_t c = 0; c < C; ++c) {
-                double s = 0.0;
-                for (int64_t i = c * kChunk; i < std::min(N, (c + 1) * kChunk); ++i) {
-                    RowScore r = score_row(f, X + (size_t)i * D, w.data(), z.data());
-                    s += r.ll;
-                    if (keep_gamma)
-                        for (int k = 0; k < K; ++k) gamma[(size_t)i * K + k] = std::exp(w[k] - r.ll);
-                }
-                part_ll[c] = s;
-            }
-        }
-        logL = 0.0;
-        for (int64_t c = 0; c < C; ++c) logL += part_ll[c];
-        return kOk;
-    };
-
     for (int t = 0; t < opts->max_iter; ++t) {
         // ---- E-step: gamma and logL_t = sum_i ll_i(theta_t)
-        if (int s = estep(cur, true)) return s;
+        if (int s = em_estep(X, N, D, K, pi, mu, cov, w, true, cur)) return s;
         per_iter[nrec++] = cur;
         if (t >= 1 && std::fabs(cur - prev) < opts->tol * (1.0 + std::fabs(cur))) {
             converged = true;  // theta_t is returned; final logL = logL_t
@@ -444,59 +533,7 @@ int eso_fit_em(const double* X, int64_t N, int D, int K, const eso_fit_opts* opt
         }
         prev = cur;
         // ---- M-step, literal two-pass form of SPEC.md:294
-#pragma omp parallel for schedule(static)
-        for (int64_t c = 0; c < C; ++c) {
-            double* nk = &part_nk[(size_t)c * K];
-            double* s1 = &part_s1[(size_t)c * K * D];
-            std::fill(nk, nk + K, 0.0);
-            std::fill(s1, s1 + (size_t)K * D, 0.0);
-            for (int64_t i = c * kChunk; i < std::min(N, (c + 1) * kChunk); ++i)
-                for (int k = 0; k < K; ++k) {
-                    double g = gamma[(size_t)i * K + k];
-                    nk[k] += g;
-                    for (int d = 0; d < D; ++d) s1[(size_t)k * D + d] += g * X[(size_t)i * D + d];
-                }
-        }
-        std::vector<double> Nk(K, 0.0);
-        for (int64_t c = 0; c < C; ++c)
-            for (int k = 0; k < K; ++k) Nk[k] += part_nk[(size_t)c * K + k];
-        for (int k = 0; k < K; ++k) {
-            for (int d = 0; d < D; ++d) {
-                double s = 0.0;
-                for (int64_t c = 0; c < C; ++c) s += part_s1[(size_t)c * K * D + (size_t)k * D + d];
-                mu[(size_t)k * D + d] = Nk[k] > 0 ? s / Nk[k] : mu[(size_t)k * D + d];
-            }
-            pi[k] = Nk[k] / (double)N;
-        }
-#pragma omp parallel
-        {
-            std::vector<double> y(D);
-#pragma omp for schedule(static)
-            for (int64_t c = 0; c < C; ++c) {
-                double* s2 = &part_s2[(size_t)c * K * D * D];
-                std::fill(s2, s2 + (size_t)K * D * D, 0.0);
-                for (int64_t i = c * kChunk; i < std::min(N, (c + 1) * kChunk); ++i)
-                    for (int k = 0; k < K; ++k) {
-                        double g = gamma[(size_t)i * K + k];
-                        for (int d = 0; d < D; ++d) y[d] = X[(size_t)i * D + d] - mu[(size_t)k * D + d];
-                        for (int a = 0; a < D; ++a)
-                            for (int b = a; b < (diag ? a + 1 : D); ++b)
-                                s2[(size_t)k * D * D + (size_t)a * D + b] += g * y[a] * y[b];
-                    }
-            }
-        }
-        for (int k = 0; k < K; ++k) {
-            double* ck = cov + (size_t)k * D * D;
-            for (int a = 0; a < D; ++a)
-                for (int b = a; b < D; ++b) {
-                    double s = 0.0;
-                    for (int64_t c = 0; c < C; ++c) s += part_s2[(size_t)c * K * D * D + (size_t)k * D * D + (size_t)a * D + b];
-                    double v = Nk[k] > 0 ? s / Nk[k] : 0.0;
-                    if (diag && a != b) v = 0.0;
-                    ck[(size_t)a * D + b] = v + (a == b ? reg : 0.0);
-                    ck[(size_t)b * D + a] = ck[(size_t)a * D + b];
-                }
-        }
+        em_mstep(X, N, D, K, reg, diag, pi, mu, cov, w, Nk);
         // ---- collapse handling: N*pi_k < 1 -> reseed
         bool any = false;
         for (int k = 0; k < K; ++k) {
@@ -519,7 +556,7 @@ int eso_fit_em(const double* X, int64_t N, int D, int K, const eso_fit_opts* opt
     }
     double final_ll = cur;
     if (!converged) {
-        if (int s = estep(final_ll, false)) return s;
+        if (int s = em_estep(X, N, D, K, pi, mu, cov, w, false, final_ll)) return s;
     }
     if (rep) {
         rep->iterations = iterations;
@@ -529,6 +566,28 @@ int eso_fit_em(const double* X, int64_t N, int D, int K, const eso_fit_opts* opt
         rep->n_per_iter = nrec;
         rep->collapses = collapses;
         rep->reg_used = reg;
+    }
+    return kOk;
+}
+
+// One EM iteration in place (bench.py --impl reference: the timed unit of the metric): the
+// E-step of fit_em and its literal two-pass M-step, no collapse reseed (collapsed components
+// are counted in *n_collapsed).  Work buffers persist per thread across calls.
+int eso_em_step(const double* X, int64_t N, int D, int K, double reg, int cov_type, double* pi, double* mu,
+                double* cov, double* logL, int* n_collapsed, int nthreads) {
+    if (K < 1 || N < K) return fail(kData, "TooFewPoints", "em_step requires N >= K >= 1");
+    set_threads(nthreads);
+    static thread_local EmWork w;
+    w.size(N, D, K);
+    std::vector<double> Nk;
+    double ll = 0.0;
+    if (int s = em_estep(X, N, D, K, pi, mu, cov, w, true, ll)) return s;
+    em_mstep(X, N, D, K, reg, cov_type == 1, pi, mu, cov, w, Nk);
+    if (logL) *logL = ll;
+    if (n_collapsed) {
+        int c = 0;
+        for (int k = 0; k < K; ++k) c += Nk[k] < 1.0;
+        *n_collapsed = c;
     }
     return kOk;
 }

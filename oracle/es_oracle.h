@@ -81,6 +81,12 @@ int eso_fit_em(const double* X, int64_t N, int D, int K, const eso_fit_opts* opt
                const double* pi_init, const double* mu_init, const double* cov_init,
                double* pi, double* mu, double* cov, eso_fit_report* rep, double* per_iter);
 
+/* One EM iteration in place (E-step + literal two-pass M-step of eso_fit_em, no
+ * collapse reseed): the timed unit of bench.py --impl reference.  *logL = logL of
+ * the parameters on entry; *n_collapsed = components with N_k < 1. */
+int eso_em_step(const double* X, int64_t N, int D, int K, double reg, int cov_type, double* pi, double* mu,
+                double* cov, double* logL, int* n_collapsed, int nthreads);
+
 /* detect: mode 0 = best-component density (Def. 1), mode 1 =
  * mixture density.  flag iff log p < log_delta.                */
 int eso_detect(const double* X, int64_t N, int D, const double* pi, const double* mu,

@@ -156,6 +156,20 @@ def fit_em(X, K, init="kmeans++", tol=1e-6, max_iter=200, reg=None, seed=0, init
     return pi, mu, cov, report
 
 
+def em_step(X, pi, mu, cov, reg, nthreads=0, covariance_type="full"):
+    """One EM iteration in place on (pi, mu, cov) (C-contiguous float64 arrays, updated);
+    returns (logL of the entry parameters, number of components with N_k < 1)."""
+    X = np.ascontiguousarray(X, np.float64)
+    N, D = X.shape
+    K = pi.shape[0]
+    for a in (pi, mu, cov):
+        assert a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]
+    ll, nc = C.c_double(), C.c_int()
+    _check(lib().eso_em_step(_p(X), C.c_int64(N), D, K, C.c_double(reg), {"full": 0, "diag": 1}[covariance_type],
+                             _p(pi), _p(mu), _p(cov), C.byref(ll), C.byref(nc), nthreads))
+    return ll.value, nc.value
+
+
 def detect(X, pi, mu, cov, log_delta, mode=0, nthreads=0):
     pi, mu, cov, K, D = _params(pi, mu, cov)
     X = np.ascontiguousarray(X, np.float64)

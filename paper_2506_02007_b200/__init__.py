@@ -267,12 +267,14 @@ class Dataset:
         return cls(ctx, h)
 
     @classmethod
-    def generate(cls, seed: int, n_global: int, D: int, K_true: int, ctx: Optional[Context] = None) -> "Dataset":
-        """SYN-v1 synthetic events generated on the device (this rank's shard)."""
+    def generate(cls, seed: int, n_global: int, D: int, K_true: int, ctx: Optional[Context] = None,
+                 row0: int = 0) -> "Dataset":
+        """SYN-v1 synthetic events generated on the device (this rank's shard); row0 > 0
+        selects rows [row0, row0 + n_global) of the same stream."""
         ctx = ctx or default_context()
         h = C.c_void_p()
-        _check(ctx._lib.es_dataset_generate(ctx.handle, C.c_uint64(seed), C.c_int64(n_global), C.c_int32(D),
-                                            C.c_int32(K_true), C.byref(h)))
+        _check(ctx._lib.es_dataset_generate_range(ctx.handle, C.c_uint64(seed), C.c_int64(row0), C.c_int64(n_global),
+                                                  C.c_int32(D), C.c_int32(K_true), C.byref(h)))
         return cls(ctx, h)
 
     def read_rows(self, row0: int = 0, n: Optional[int] = None, out=None):

@@ -1179,7 +1179,8 @@ __device__ bool chol_inv_warp(const double* A, double* L, double* W, int D, doub
         for (int p = lane; p < j; p += 32) s = fma(L[j * D + p], L[j * D + p], s);
         s = warp_sum(s);
         const double dj = A[j * D + j] - s;
-        if (!(dj > 0.0) || !isfinite(dj)) ok = false;
+        // numerical singularity: pivot at or below D 2^-46 of its diagonal entry (as the oracle)
+        if (!(dj > ldexp((double)D, -46) * A[j * D + j]) || !isfinite(dj)) ok = false;
         const double ljj = sqrt(fmax(dj, 0.0));
         __syncwarp();
         if (lane == 0) L[j * D + j] = ljj;

@@ -502,7 +502,11 @@ struct Out {
 void score_launch(es_ctx* c, const double* X, int64_t n, int64_t ld, int D, int K, const double* dmodel,
                   const double* center, const double* center_host, double xs, const ScoreOut& o, double* bs,
                   int* nblk, const CUtensorMap* xmap = nullptr) {
-    if (c->precision == 0 && center && center_host && xmap && score_mma_enabled(D, K, o))
+    // mixture mode decides on ll itself: flags and calibration keys at the
+    // threshold then need ll to FP64 accuracy, so that ablation scores on the strict kernel
+    if (o.mode == 1)
+        launch_score(X, n, ld, D, K, dmodel, o, bs, c->num_sms, nblk, c->stream, c->ls);
+    else if (c->precision == 0 && center && center_host && xmap && score_mma_enabled(D, K, o))
         launch_score_mma(xmap, n, D, K, dmodel, center, center_host, xs, o, bs, c->num_sms, nblk, c->stream,
                          c->ls);
     else if (c->precision == 0 && center && xmap && score_tc_supported(D, K, o))
@@ -1122,14 +1126,19 @@ static void syn_true_model(uint64_t seed, int D, int K, std::vector<double>& cum
 }
 
 int es_dataset_generate(es_ctx* c, uint64_t seed, int64_t n_global, int32_t D, int32_t K_true, es_dataset** out) {
+    return es_dataset_generate_range(c, seed, 0, n_global, D, K_true, out);
+}
+
+int es_dataset_generate_range(es_ctx* c, uint64_t seed, int64_t row0, int64_t n_global, int32_t D, int32_t K_true,
+                              es_dataset** out) {
     return guard([&] {
         if (D < 1 || D > 64) fail(ES_ERR_DATA, "DimensionMismatch", "D must be in [1,64]");
-        if (K_true < 1 || n_global < 0) fail(ES_ERR_DATA, "RangeViolation", "bad generator shape");
+        if (K_true < 1 || n_global < 0 || row0 < 0) fail(ES_ERR_DATA, "RangeViolation", "bad generator shape");
         CU(cudaSetDevice(c->device));
         auto ds = std::make_unique<es_dataset>();
         ds->ctx = c;
         ds->D = D;
-        const int64_t r0 = n_global * c->rank / c->world, r1 = n_global * (c->rank + 1) / c->world;
+        const int64_t r0 = row0 + n_global * c->rank / c->world, r1 = row0 + n_global * (c->rank + 1) / c->world;
         ds->n_local = r1 - r0;
         ds->ld = plane_ld(std::max<int64_t>(ds->n_local, 1));
         CU(cudaMalloc(&ds->X, (size_t)ds->ld * D * 8));
@@ -1698,6 +1707,7 @@ int es_gmm_calibrate(es_ctx* c, es_dataset* ds, const es_gmm_params* p, int64_t 
         double* keys = c->out_scratch.as<double>(std::max<int64_t>(nloc, 1));
         if (nloc > 0) {  // the train rows are the first nloc local rows (planes keep their stride)
             ScoreOut o;
+            o.mode = mode;
             if (mode == 1) o.ll = keys;
             else o.best_ld = keys;
             int nblk = 0;

@@ -233,3 +233,18 @@ def test_syn_v1_shape_and_ratio(oracle):
     # counter-based: any sub-range regenerates identically
     X2, _, _ = oracle.syn_rows(42, 8, 4, model, 1234, 10)
     assert np.array_equal(X2, X[1234:1244])
+
+
+def test_em_step_is_one_fit_iteration(oracle):
+    # bench.py --impl reference times eso_em_step: one iteration of eso_fit_em exactly
+    model = oracle.syn_model(42, 4, 3)
+    X, _, _ = oracle.syn_rows(42, 4, 3, model, 0, 20_000)
+    pi, mu, cov, reg = oracle.random_init(X, 3, 7)
+    p2, m2, c2, rep = oracle.fit_em(X, 3, init_params=(pi, mu, cov), tol=0.0, max_iter=2, reg=reg)
+    lls = []
+    for _ in range(2):
+        ll, nc = oracle.em_step(X, pi, mu, cov, reg)
+        lls.append(ll)
+        assert nc == 0
+    assert np.array_equal(pi, p2) and np.array_equal(mu, m2) and np.array_equal(cov, c2)
+    assert lls == list(rep["per_iteration_log_likelihoods"])
