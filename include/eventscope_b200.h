@@ -119,6 +119,9 @@ int es_ctx_destroy(es_ctx* ctx);
 int es_ctx_stream(es_ctx* ctx, void** stream);
 /* Kernel-launch counter (for launch accounting in benchmarks). */
 int es_ctx_launch_count(es_ctx* ctx, int64_t* count);
+/* NCCL collectives this context issued (0 for a single-GPU context; a context made by
+ * es_ctx_create_nccl, including a one-rank one under ES_FORCE_NCCL=1, exchanges through NCCL). */
+int es_ctx_collective_count(es_ctx* ctx, int64_t* count);
 /* Arithmetic of the hot kernels: 0 (default) = mixed — FP32 whitening, FP64
  * statistics / log-likelihoods, FP64 recomputation of every component that
  * can change an output at the 1e-6 level; 1 = strict FP64 everywhere. */

@@ -211,6 +211,13 @@ class Context:
         _check(self._lib.es_ctx_launch_count(self.handle, C.byref(n)))
         return n.value
 
+    @property
+    def collective_count(self) -> int:
+        """NCCL collectives this context issued."""
+        n = C.c_int64()
+        _check(self._lib.es_ctx_collective_count(self.handle, C.byref(n)))
+        return n.value
+
     def close(self) -> None:
         if getattr(self, "handle", None):
             self._lib.es_ctx_destroy(self.handle)
@@ -446,8 +453,10 @@ def mixture_density(model: GmmModel, x, ctx: Optional[Context] = None) -> float:
 
 def detect(model: GmmModel, X, delta: Optional[float] = None, mode: str = "component",
            log_delta: Optional[float] = None, ctx: Optional[Context] = None, flags=None, best_k=None,
-           best_logdens=None, indices: bool = True) -> DetectionReport:
-    """Def. 1 / Alg. 2: flag iff log p < log delta (strict)."""
+           best_logdens=None, indices=True) -> DetectionReport:
+    """Def. 1 / Alg. 2: flag iff log p < log delta (strict).
+    flags / best_k / best_logdens / indices may be caller buffers (numpy or CUDA tensors; a
+    device buffer keeps that output in HBM); indices=False skips the anomaly-index list."""
     if log_delta is None:
         if delta is None or not delta > 0:
             raise EventscopeError("Data", "RangeViolation", "delta must be > 0")
@@ -458,14 +467,19 @@ def detect(model: GmmModel, X, delta: Optional[float] = None, mode: str = "compo
     fl = np.empty(n, np.uint8) if flags is None else flags
     bk = np.empty(n, np.int32) if best_k is None else best_k
     bl = np.empty(n) if best_logdens is None else best_logdens
-    idx = np.empty(max(n, 1), np.int64) if indices else None
+    if indices is True:
+        idx = np.empty(max(n, 1), np.int64)
+    elif indices is False or indices is None:
+        idx = None
+    else:
+        idx = indices  # caller buffer, capacity >= n_local
     nloc, ng = C.c_int64(), C.c_int64()
     m = {"component": 0, "mixture": 1}[mode]
     _check(ds.ctx._lib.es_gmm_detect(ds.ctx.handle, ds.handle, C.byref(p), C.c_double(log_delta), C.c_int32(m),
                                      C.c_void_p(_ptr(fl)), C.c_void_p(_ptr(bk)), C.c_void_p(_ptr(bl)),
                                      C.c_void_p(_ptr(idx)), C.byref(nloc), C.byref(ng)))
     del keep
-    A = idx[:nloc.value].copy() if indices else np.zeros(0, np.int64)
+    A = np.zeros(0, np.int64) if idx is None else (idx[:nloc.value].copy() if indices is True else idx[:nloc.value])
     d = float(np.exp(log_delta)) if delta is None else float(delta)
     return DetectionReport(fl, A, bk, bl, model, d, float(log_delta), ng.value)
 

@@ -250,16 +250,21 @@ void launch_col_stats(const double* X, int64_t n, int64_t ld, int D, double* scr
 }
 
 // ======================================================= fixed-order reduce
+// One warp per output entry: lane l sums blocks l, l + 32, ... in order, then a fixed xor
+// tree across the lanes (deterministic; ~5 loads deep instead of a 148-long serial chain).
 __global__ void k_reduce_blocks(const double* __restrict__ partial, int nblk, int len, double* __restrict__ out) {
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
     if (e >= len) return;
     double s = 0.0;
-    for (int b = 0; b < nblk; ++b) s += partial[(int64_t)b * len + e];
-    out[e] = s;
+#pragma unroll 4
+    for (int b = lane; b < nblk; b += 32) s += partial[(int64_t)b * len + e];
+    s = warp_sum(s);
+    if (lane == 0) out[e] = s;
 }
 
 void launch_reduce_blocks(const double* partial, int nblk, int len, double* out, cudaStream_t s, LaunchStats& ls) {
-    k_reduce_blocks<<<(len + 127) / 128, 128, 0, s>>>(partial, nblk, len, out);
+    k_reduce_blocks<<<(len + 7) / 8, 256, 0, s>>>(partial, nblk, len, out);
     ++ls.launches;
 }
 

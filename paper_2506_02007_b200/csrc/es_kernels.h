@@ -21,6 +21,7 @@ struct ScoreOut {
     double* lnk = nullptr;         // n x K component log densities
     double log_delta = 0.0;
     int mode = 0;                  // 0 component, 1 mixture
+    int sum_ll = 1;                // the per-CTA sum of ll is used (0: detect / calibrate skip ll)
 };
 
 struct LaunchStats {

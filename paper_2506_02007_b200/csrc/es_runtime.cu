@@ -175,6 +175,7 @@ struct es_ctx {
     cudaEvent_t evc[2] = {nullptr, nullptr}, evt[2] = {nullptr, nullptr};
     int num_sms = 148;
     LaunchStats ls;
+    int64_t collectives = 0;  // NCCL collectives issued (replays of captured ones included)
     DevBuf stage2;  // second staging buffer of dataset_create
     // the planes of the last destroyed dataset, kept for the next dataset_create of a
     // similar size (an 8.6 GB cudaMalloc / cudaFree pair per fit-on-fresh-data call is
@@ -210,28 +211,41 @@ struct es_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double em_ms = 0.0, score_ms = 0.0;
     int64_t em_launches = 0, score_launches = 0;
+    double* t_acc = nullptr;  // measurement pending until the next stream synchronisation
+    int64_t* t_cnt = nullptr;
     void t_begin() {
         if (timing) CU(cudaEventRecord(ev0, stream));
     }
+    // records the end event only: the elapsed time is collected after the next sync(), so
+    // timing adds no host round trip inside an EM iteration
     void t_end(double& acc, int64_t& cnt) {
         if (!timing) return;
         CU(cudaEventRecord(ev1, stream));
-        CU(cudaEventSynchronize(ev1));
+        t_acc = &acc;
+        t_cnt = &cnt;
+    }
+    void t_collect() {
+        if (!t_acc) return;
         float ms = 0.f;
         CU(cudaEventElapsedTime(&ms, ev0, ev1));
-        acc += ms;
-        ++cnt;
+        *t_acc += ms;
+        ++*t_cnt;
+        t_acc = nullptr;
     }
 
-    void sync() { CU(cudaStreamSynchronize(stream)); }
+    void sync() {
+        CU(cudaStreamSynchronize(stream));
+        t_collect();
+    }
     void check_launch() { CU(cudaGetLastError()); }
 
     // All-gather count doubles per rank (device in/out).
     void allgather(const double* d_send, double* d_recv, size_t count) {
-        if (world == 1) {
+        if (world == 1 && mode != 1) {
             if (d_send != d_recv) CU(cudaMemcpyAsync(d_recv, d_send, count * 8, cudaMemcpyDeviceToDevice, stream));
         } else if (mode == 1) {
             NC(nccl().AllGather(d_send, d_recv, count, ncclFloat64, comm, stream));
+            ++collectives;
         } else {
             std::vector<double> s(count), r(count * world);
             CU(cudaMemcpyAsync(s.data(), d_send, count * 8, cudaMemcpyDeviceToHost, stream));
@@ -244,7 +258,7 @@ struct es_ctx {
     }
     // In-place all-reduce on HOST memory (small control values).
     void allreduce_host(void* buf, size_t count, int dtype, int op) {
-        if (world == 1) return;
+        if (world == 1 && mode != 1) return;
         if (mode == 2) {
             if (ex.allreduce(ex.user, buf, count, dtype, op) != 0)
                 fail(ES_ERR_RUNTIME, "ExchangeError", "allreduce callback failed");
@@ -256,13 +270,14 @@ struct es_ctx {
         const ncclDataType_t t = dtype == 0 ? ncclFloat64 : ncclInt64;
         const ncclRedOp_t o = op == 0 ? ncclSum : op == 1 ? ncclMin : ncclMax;
         NC(nccl().AllReduce(d, d, count, t, o, comm, stream));
+        ++collectives;
         CU(cudaMemcpyAsync(buf, d, bytes, cudaMemcpyDeviceToHost, stream));
         sync();
     }
     // Rank-ordered all-gather of host values.
     std::vector<double> allgather_host(const double* v, size_t count) {
         std::vector<double> r(count * world);
-        if (world == 1) {
+        if (world == 1 && mode != 1) {
             std::copy(v, v + count, r.begin());
             return r;
         }
@@ -274,6 +289,7 @@ struct es_ctx {
         double* d = xbuf.as<double>(count * (world + 1));
         CU(cudaMemcpyAsync(d, v, count * 8, cudaMemcpyHostToDevice, stream));
         NC(nccl().AllGather(d, d + count, count, ncclFloat64, comm, stream));
+        ++collectives;
         CU(cudaMemcpyAsync(r.data(), d + count, count * world * 8, cudaMemcpyDeviceToHost, stream));
         sync();
         return r;
@@ -319,6 +335,20 @@ struct es_em_state {
     int collapses = 0;
     bool converged = false, done = false;
     double prev = 0.0, last = 0.0;
+    // the fit's own device buffers (sized once in em_begin, so the pointers a captured
+    // iteration graph holds stay valid for the whole fit) and the graphs per iteration path
+    DevBuf model, backup, partial, stats_local, stats_all, status;
+    size_t part_cap = 0;
+    struct Graph {
+        int key;
+        cudaGraphExec_t exec;
+        int64_t launches;     // kernels in one replay (launch accounting)
+        int64_t collectives;  // NCCL collectives in one replay
+    };
+    std::vector<Graph> graphs;
+    ~es_em_state() {
+        for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+    }
 };
 
 // ============================================================== helpers
@@ -676,7 +706,7 @@ void em_init_model(es_em_state* st, const es_gmm_params* init, const DataStats& 
                         (is_diag(st) && a != b) ? 0.0 : dsx.S[(size_t)a * D + b] + (a == b ? st->reg : 0.0);
         }
     }
-    double* m = c->model.as<double>(mstride(K, D));
+    double* m = st->model.as<double>(mstride(K, D));
     upload_model(c, m, K, D, pi.data(), mu.data(), cov.data());
     st->min_nk = (double)ds->n_global * *std::min_element(pi.begin(), pi.end());
 }
@@ -712,6 +742,15 @@ void em_begin(es_em_state* st, const es_gmm_params* init) {
         st->f32conv = span > 0.0 && mag <= 4.0 * span && mag < 1e30;
     }
     CU(cudaMemcpyAsync(st->dcenter.as<double>(D), dsx.mean.data(), D * 8, cudaMemcpyHostToDevice, c->stream));
+    {  // the fit's buffers at their final sizes (every iteration path), allocated once
+        const int NE1 = stat_total(D, K);
+        st->part_cap = (size_t)std::max(em_grid(D, K, c->num_sms), 2 * c->num_sms) * NE1;
+        st->partial.as<double>(st->part_cap);
+        st->stats_local.as<double>(NE1);
+        st->stats_all.as<double>((size_t)NE1 * c->world);
+        st->status.as<IterStatus>(1);
+        st->backup.as<double>(mstride(K, D));
+    }
     st->reg = st->opts.reg < 0 ? default_reg(dsx.S, D) : st->opts.reg;
     st->rng = SplitMix64(st->opts.seed);
     em_init_model(st, init, dsx);
@@ -733,11 +772,11 @@ bool em_logl_pass(es_em_state* st, double* out) {
     const int K = st->K, D = st->D;
     if (is_diag(st) || !mixed_em(c, st) || !em_mma_enabled() || !ds->has_xmap) return false;
     const int NE1 = stat_total(D, K);
-    double* dmodel = c->model.as<double>(mstride(K, D));
-    double* loc = c->stats_local.as<double>(NE1);
+    double* dmodel = st->model.as<double>(mstride(K, D));
+    double* loc = st->stats_local.as<double>(NE1);
     if (ds->n_local > 0) {
         int nblk = 0;
-        double* part = c->partial.as<double>((size_t)std::max(em_grid(D, K, c->num_sms), c->num_sms) * NE1);
+        double* part = st->partial.as<double>(st->part_cap);
         const int np = st->min_nk >= kOnePassMinNk ? 1 : 2;
         launch_em_mma(&ds->xmap, ds->n_local, D, K, dmodel, st->dcenter.as<double>(D), st->mean.data(), st->xs,
                       st->f32conv, np, part, c->num_sms, &nblk, c->stream, c->ls);
@@ -756,81 +795,214 @@ bool em_logl_pass(es_em_state* st, double* out) {
     return true;
 }
 
-// One EM iteration; returns true when the loop must stop.
-bool em_iterate(es_em_state* st) {
+// Iteration paths (the EM pass kernel and its statistics format).
+enum EmIterPath { kPathEmpty = 0, kPathDiag, kPathStrict, kPathMma1, kPathMma2, kPathWs, kPathTc, kPathFast };
+
+int em_choose_path(const es_em_state* st) {
+    es_ctx* c = st->ctx;
+    const es_dataset* ds = st->ds;
+    if (ds->n_local == 0) return kPathEmpty;
+    if (is_diag(st)) return kPathDiag;
+    if (mixed_em(c, st)) {
+        if (em_mma_enabled() && ds->has_xmap) {
+            const int np = em_mma_passes() ? em_mma_passes() : (st->min_nk >= kOnePassMinNk ? 1 : 2);
+            return np == 1 ? kPathMma1 : kPathMma2;
+        }
+        if (em_ws_enabled() && ds->has_xmap) return kPathWs;
+        if (em_tc_enabled()) return kPathTc;
+        return kPathFast;
+    }
+    return kPathStrict;
+}
+
+// Enqueues one EM iteration on the context stream, no host synchronisation:
+//   EM pass (fused E + M statistics, per-CTA partials) -> fixed-order block reduce ->
+//   rank exchange (NCCL all-gather; skipped on one rank) -> k_finalize (rank-ordered sum,
+//   M-step, Cholesky, W = L^-1, collapse flags, logL) -> 40-byte IterStatus to pinned host.
+// The EM pass of an iteration path: launches it and returns the statistics format for
+// k_finalize (*nblk = partial blocks written).
+int em_pass_launch(es_em_state* st, int path, int* nblk) {
+    es_ctx* c = st->ctx;
+    es_dataset* ds = st->ds;
+    const int K = st->K, D = st->D;
+    double* dmodel = st->model.as<double>(mstride(K, D));
+    double* part = st->partial.as<double>(st->part_cap);
+    *nblk = 0;
+    switch (path) {
+        case kPathDiag:
+            launch_em_diag(ds->X, ds->n_local, ds->ld, D, K, dmodel, part, c->num_sms, nblk, c->stream, c->ls);
+            return 2;
+        case kPathMma1:
+        case kPathMma2:
+            launch_em_mma(&ds->xmap, ds->n_local, D, K, dmodel, st->dcenter.as<double>(D), st->mean.data(), st->xs,
+                          st->f32conv, path == kPathMma1 ? 1 : 2, part, c->num_sms, nblk, c->stream, c->ls);
+            return 3;
+        case kPathWs:
+            launch_em_ws(&ds->xmap, ds->n_local, D, K, dmodel, st->dcenter.as<double>(D), part, c->num_sms, nblk,
+                         c->stream, c->ls);
+            return 0;
+        case kPathTc:
+            launch_em_tc(ds->X, ds->n_local, ds->ld, D, K, dmodel, st->dcenter.as<double>(D), part, c->num_sms,
+                         nblk, c->stream, c->ls);
+            return 0;
+        case kPathFast:
+            launch_em_fast(ds->X, ds->n_local, ds->ld, D, K, dmodel, st->dcenter.as<double>(D), part, c->num_sms,
+                           nblk, c->stream, c->ls);
+            return 0;
+        case kPathStrict: {
+            bool wh = true;
+            launch_em_pass(ds->X, ds->n_local, ds->ld, D, K, dmodel, part, c->num_sms, nblk, &wh, c->stream, c->ls);
+            return wh ? 1 : 0;
+        }
+        default:  // an empty shard announces the statistics format the other ranks use
+            if (is_diag(st)) return 2;
+            if (mixed_em(c, st)) return em_mma_enabled() ? 3 : 0;
+            return em_path(D, K) != EmPath::Generic ? 1 : 0;
+    }
+}
+
+// Everything of an iteration after the EM pass: fixed-order block reduce -> rank exchange
+// (NCCL all-gather; skipped on one rank) -> k_finalize (rank-ordered sum, M-step, Cholesky,
+// W = L^-1, collapse flags, logL) -> 40-byte IterStatus to pinned host memory.
+void em_tail_launch(es_em_state* st, int path, int nblk, int whitened) {
     es_ctx* c = st->ctx;
     es_dataset* ds = st->ds;
     const int K = st->K, D = st->D;
     const int NE1 = stat_total(D, K);
-    double* dmodel = c->model.as<double>(mstride(K, D));
-    double* backup = c->model_backup.as<double>(mstride(K, D));
-    CU(cudaMemcpyAsync(backup, dmodel, mstride(K, D) * 8, cudaMemcpyDeviceToDevice, c->stream));
-    double* loc = c->stats_local.as<double>(NE1);
-    int whitened = 1;
-    if (ds->n_local > 0 && is_diag(st)) {
-        int nblk = 0;
-        double* part = c->partial.as<double>((size_t)2 * c->num_sms * NE1);
-        c->t_begin();
-        launch_em_diag(ds->X, ds->n_local, ds->ld, D, K, dmodel, part, c->num_sms, &nblk, c->stream, c->ls);
-        c->t_end(c->em_ms, c->em_launches);
+    double* dmodel = st->model.as<double>(mstride(K, D));
+    double* part = st->partial.as<double>(st->part_cap);
+    double* loc = st->stats_local.as<double>(NE1);
+    if (path != kPathEmpty)
         launch_reduce_blocks(part, nblk, NE1, loc, c->stream, c->ls);
-        whitened = 2;
-    } else if (ds->n_local > 0) {
-        int nblk = 0;
-        double* part = c->partial.as<double>((size_t)std::max(em_grid(D, K, c->num_sms), c->num_sms) * NE1);
-        c->t_begin();
-        bool wh = true, wh_mma = false;
-        st->last_npass = 0;
-        if (mixed_em(c, st)) {
-            if (em_mma_enabled() && ds->has_xmap) {
-                const int np = st->min_nk >= kOnePassMinNk ? 1 : 2;
-                launch_em_mma(&ds->xmap, ds->n_local, D, K, dmodel, st->dcenter.as<double>(D), st->mean.data(),
-                              st->xs, st->f32conv, np, part, c->num_sms, &nblk, c->stream, c->ls);
-                st->last_npass = em_mma_passes() ? em_mma_passes() : np;
-                wh_mma = true;
-            } else if (em_ws_enabled() && ds->has_xmap)
-                launch_em_ws(&ds->xmap, ds->n_local, D, K, dmodel, st->dcenter.as<double>(D), part, c->num_sms,
-                             &nblk, c->stream, c->ls);
-            else if (em_tc_enabled())
-                launch_em_tc(ds->X, ds->n_local, ds->ld, D, K, dmodel, st->dcenter.as<double>(D), part, c->num_sms,
-                             &nblk, c->stream, c->ls);
-            else
-                launch_em_fast(ds->X, ds->n_local, ds->ld, D, K, dmodel, st->dcenter.as<double>(D), part,
-                               c->num_sms, &nblk, c->stream, c->ls);
-            wh = false;
-        } else {
-            launch_em_pass(ds->X, ds->n_local, ds->ld, D, K, dmodel, part, c->num_sms, &nblk, &wh, c->stream,
-                           c->ls);
-        }
-        whitened = wh_mma ? 3 : (wh ? 1 : 0);
-        c->t_end(c->em_ms, c->em_launches);
-        launch_reduce_blocks(part, nblk, NE1, loc, c->stream, c->ls);
-    } else {
+    else
         CU(cudaMemsetAsync(loc, 0, NE1 * 8, c->stream));
-        // an empty shard must announce the same statistics format as the others
-        if (is_diag(st))
-            whitened = 2;
-        else if (mixed_em(c, st))
-            whitened = em_mma_enabled() ? 3 : 0;
-        else
-            whitened = em_path(D, K) != EmPath::Generic ? 1 : 0;
+    const double* all = loc;
+    if (c->world > 1 || c->mode == 1) {
+        double* ag = st->stats_all.as<double>((size_t)NE1 * c->world);
+        c->allgather(loc, ag, NE1);
+        all = ag;
     }
-    double* all = c->stats_all.as<double>((size_t)NE1 * c->world);
-    c->allgather(loc, all, NE1);
-    IterStatus* dst = c->status.as<IterStatus>(1);
+    IterStatus* dst = st->status.as<IterStatus>(1);
     CU(cudaMemsetAsync(dst, 0, sizeof(IterStatus), c->stream));
     launch_finalize(all, c->world, D, K, ds->n_global, st->reg, whitened, dmodel, dst, nullptr, st->t, c->stream,
                     c->ls, st->dcenter.as<double>(D), st->xs);
     c->check_launch();
     CU(cudaMemcpyAsync(c->h_status, dst, sizeof(IterStatus), cudaMemcpyDeviceToHost, c->stream));
+}
+
+// Captures whatever `enqueue` puts on the context stream as a graph (launch and collective
+// accounting per replay).
+template <class F>
+es_em_state::Graph capture_graph(es_ctx* c, int key, F&& enqueue) {
+    cudaGraph_t graph = nullptr;
+    const int64_t l0 = c->ls.launches, n0 = c->collectives;
+    CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
+    try {
+        enqueue();
+    } catch (...) {
+        cudaStreamEndCapture(c->stream, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        c->ls.launches = l0;
+        c->collectives = n0;
+        throw;
+    }
+    CU(cudaStreamEndCapture(c->stream, &graph));
+    cudaGraphExec_t ex = nullptr;
+    const cudaError_t e = cudaGraphInstantiate(&ex, graph, 0);
+    cudaGraphDestroy(graph);
+    CU(e);
+    es_em_state::Graph g{key, ex, c->ls.launches - l0, c->collectives - n0};
+    c->ls.launches = l0;
+    c->collectives = n0;
+    return g;
+}
+
+// ES_GRAPH=0 disables the per-path CUDA graph of the iteration (default on; never in the
+// host-exchange mode, whose all-gather is a host callback).
+bool graphs_enabled(const es_ctx* c) {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ES_GRAPH");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1 && c->mode != 2;
+}
+
+// One EM iteration (graph replays, or the same sequence launched directly) and the single
+// host synchronisation of the loop: the IterStatus read.  Timing mode records ev0 / ev1 on
+// the stream around the EM pass (a separate graph), so the pass is timed live.
+void em_run_iteration(es_em_state* st, int path) {
+    es_ctx* c = st->ctx;
+    const bool timed = c->timing && path != kPathEmpty;
+    if (!graphs_enabled(c)) {
+        int nblk = 0;
+        if (timed) c->t_begin();
+        const int wh = em_pass_launch(st, path, &nblk);
+        if (timed) c->t_end(c->em_ms, c->em_launches);
+        em_tail_launch(st, path, nblk, wh);
+        c->sync();
+        return;
+    }
+    auto find = [&](int key) -> es_em_state::Graph* {
+        for (auto& x : st->graphs)
+            if (x.key == key) return &x;
+        return nullptr;
+    };
+    auto replay = [&](es_em_state::Graph* g) {
+        CU(cudaGraphLaunch(g->exec, c->stream));
+        c->ls.launches += g->launches;
+        c->collectives += g->collectives;
+    };
+    if (!timed) {  // key path: one graph for the whole iteration
+        es_em_state::Graph* g = find(4 * path);
+        if (!g) {
+            st->graphs.push_back(capture_graph(c, 4 * path, [&] {
+                int nblk = 0;
+                const int wh = em_pass_launch(st, path, &nblk);
+                em_tail_launch(st, path, nblk, wh);
+            }));
+            g = &st->graphs.back();
+        }
+        replay(g);
+    } else {  // key 4 path + 1: the pass, 4 path + 2: the tail
+        es_em_state::Graph* gp = find(4 * path + 1);
+        es_em_state::Graph* gt = find(4 * path + 2);
+        if (!gp || !gt) {
+            int nblk = 0, wh = 0;
+            st->graphs.push_back(capture_graph(c, 4 * path + 1, [&] { wh = em_pass_launch(st, path, &nblk); }));
+            st->graphs.push_back(capture_graph(c, 4 * path + 2, [&] { em_tail_launch(st, path, nblk, wh); }));
+            gp = find(4 * path + 1);
+            gt = find(4 * path + 2);
+        }
+        c->t_begin();
+        replay(gp);
+        c->t_end(c->em_ms, c->em_launches);
+        replay(gt);
+    }
     c->sync();
+}
+
+// One EM iteration; returns true when the loop must stop.
+bool em_iterate(es_em_state* st) {
+    es_ctx* c = st->ctx;
+    es_dataset* ds = st->ds;
+    const int K = st->K, D = st->D;
+    double* dmodel = st->model.as<double>(mstride(K, D));
+    double* backup = st->backup.as<double>(mstride(K, D));
+    // theta_t is returned on convergence: keep it (never needed when tol <= 0)
+    const bool can_converge = st->opts.tol > 0.0;
+    if (can_converge)
+        CU(cudaMemcpyAsync(backup, dmodel, mstride(K, D) * 8, cudaMemcpyDeviceToDevice, c->stream));
+    const int path = em_choose_path(st);
+    st->last_npass = path == kPathMma1 ? 1 : path == kPathMma2 ? 2 : 0;
+    em_run_iteration(st, path);
     const IterStatus s = *c->h_status;
     const double cur = s.logL;
     if (s.min_nk_inv) st->min_nk = __builtin_bit_cast(double, ~(unsigned long long)s.min_nk_inv);
     st->per_iter.push_back(cur);
     st->last = cur;
     const int t = st->t++;
-    if (t >= 1 && std::fabs(cur - st->prev) < st->opts.tol * (1.0 + std::fabs(cur))) {
+    if (can_converge && t >= 1 && std::fabs(cur - st->prev) < st->opts.tol * (1.0 + std::fabs(cur))) {
         // converged: theta_t (before this M-step) is returned, final logL = logL_t
         CU(cudaMemcpyAsync(dmodel, backup, mstride(K, D) * 8, cudaMemcpyDeviceToDevice, c->stream));
         c->sync();
@@ -976,6 +1148,10 @@ int es_ctx_stream(es_ctx* c, void** stream) {
 
 int es_ctx_launch_count(es_ctx* c, int64_t* count) {
     return guard([&] { *count = c->ls.launches; });
+}
+
+int es_ctx_collective_count(es_ctx* c, int64_t* count) {
+    return guard([&] { *count = c->collectives; });
 }
 
 int es_ctx_set_precision(es_ctx* c, int mode) {
@@ -1535,7 +1711,7 @@ int es_gmm_em_end(es_em_state* st, es_gmm_params* out, es_fit_report* rep, doubl
         es_ctx* c = st->ctx;
         CU(cudaSetDevice(c->device));
         const int K = st->K, D = st->D;
-        double* dmodel = c->model.as<double>(mstride(K, D));
+        double* dmodel = st->model.as<double>(mstride(K, D));
         double final_ll = st->last;
         if (!st->converged && !em_logl_pass(st, &final_ll))
             final_ll = run_score(c, st->ds, dmodel, K, ScoreOut{}, st->dcenter.as<double>(D), st->mean.data(), st->xs);
@@ -1672,6 +1848,7 @@ int es_gmm_detect(es_ctx* c, es_dataset* ds, const es_gmm_params* p, double log_
         o.best_ld = o_bl.dev;
         o.log_delta = log_delta;
         o.mode = mode;
+        o.sum_ll = 0;  // detect reports no log-likelihood
         run_score(c, ds, m, p->K, o, c->center.as<double>(ds->D), c->center_host.data(), c->center_xs);
         int64_t* cnt = c->scratch2.as<int64_t>((n + 4095) / 4096 + 2);
         int64_t* dcount = cnt + (n + 4095) / 4096 + 1;
@@ -1708,6 +1885,7 @@ int es_gmm_calibrate(es_ctx* c, es_dataset* ds, const es_gmm_params* p, int64_t 
         if (nloc > 0) {  // the train rows are the first nloc local rows (planes keep their stride)
             ScoreOut o;
             o.mode = mode;
+            o.sum_ll = 0;
             if (mode == 1) o.ll = keys;
             else o.best_ld = keys;
             int nblk = 0;

@@ -26,9 +26,20 @@
 
 namespace es {
 
+#ifdef ES_SCORE_COUNT
+__device__ unsigned long long g_score_pairs;
+#endif
+
 namespace {
 
 using namespace mma;
+
+// MUFU square root (relative error ~2^-22): feeds only the error bounds
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 
 #ifndef ES_SCORE_NWG  // 3: 7.3 ms per 2^26-event pass; 2 (168 registers): 8.0 ms
 #define ES_SCORE_NWG 3
@@ -50,9 +61,9 @@ struct SmemS {
     double wred[4 * NWG][2];
     unsigned char bw[2][OPB];
     unsigned char bb[OPB];
-    uint8_t cev[NWG][4 * (KMAX * 32 + KMAX)];    // compacted candidates per warp (component-major): event
-    uint8_t ccomp[NWG][4 * (KMAX * 32 + KMAX)];  //                                                component
+    uint16_t plist[NWG][4 * 256];                // extra (event << 4 | component) pairs per warp
     float cst[KMAX], lnf[KMAX], hq[KMAX], tk[KMAX];
+    float ec1[KMAX], ec0[KMAX];  // error-bound constants: eps1 ||B_k||_F, eps2 ||b^_k||_2 (U / t_k units)
     uint64_t xfull[XS], xfree[XS], aeready[NWG], edone[NWG], efree;
     uint32_t tmem;
 };
@@ -75,6 +86,25 @@ __global__ void __launch_bounds__(NTHR, 1) k_score_mma(const __grid_constant__ C
     for (int j = t; j < DM; j += NTHR) S.c[j] = j < D ? center[j] : 0.0;
     for (int e = t; e < XS * DM * TM; e += NTHR) (&S.xd[0][0])[e] = 0.0;  // planes >= D stay zero
     stage_estep(mv, K, D, center, S.c, xs, S.bw[0], S.bw[1], S.bb, S.cst, S.lnf, S.hq, S.tk, t, NTHR);
+    __syncthreads();
+    if (t < KMAX) {  // error-bound constants of the 3 x fp16 whitening (see the candidate selection)
+        double nB = 0.0, nb = 0.0;
+        if (t < K) {
+            const double* W = mv.W() + (int64_t)t * D * D;
+            const double it = 1.0 / (double)S.tk[t];
+            for (int a = 0; a < D; ++a) {
+                double b = 0.0;
+                for (int f = 0; f <= a; ++f) {
+                    const double w = W[a * D + f] / xs * it;
+                    nB += w * w;
+                    b = fma(W[a * D + f], mv.mu()[t * D + f] - S.c[f], b);
+                }
+                nb += (b * it) * (b * it);
+            }
+        }
+        S.ec1[t] = (float)(0x1p-19 * sqrt(nB));
+        S.ec0[t] = (float)(0x1p-22 * sqrt(nb));
+    }
     for (int e = t; e < KMAX * DM * DM; e += NTHR) {  // transposed: WT[k][f][r] = W_k[r][f]
         const int k = e / (DM * DM), fr = e % (DM * DM), f = fr / DM, r = fr % DM;
         S.W64[k * W64S + fr] = (k < K && r < D && f < D) ? mv.W()[(int64_t)k * D * D + r * D + f] : 0.0;
@@ -124,28 +154,26 @@ __global__ void __launch_bounds__(NTHR, 1) k_score_mma(const __grid_constant__ C
         const int p = t & 127;
         const int q = warp & 3;
         const uint32_t lq = (uint32_t)(32 * q) << 16;
-        const unsigned lt_mask = (1u << lane) - 1u;
-        float cst[KMAX], lnf[KMAX], hq[KMAX];
-#pragma unroll
-        for (int k = 0; k < KMAX; ++k) {
-            cst[k] = S.cst[k];
-            lnf[k] = S.lnf[k];
-            hq[k] = S.hq[k];
-        }
-        const float ldf = (float)o.log_delta;
+        // per-component constants are read from shared memory (broadcast) where used: kept in
+        // registers they would be live across the FP64 refinement (register spills)
+        const float* cst = S.cst;
+        const float* lnf = S.lnf;
+        const float* hq = S.hq;
+        float xnorm = 0.f, xnorm_next = 0.f;  // ||x^||_2 of this thread's event (error bound)
         double ll_acc = 0.0, nflag = 0.0;
         // convert tile j; returns whether this event left the fp16-safe range of x^ (then
         // every component of the event is refined in FP64: its FP32 densities are not used)
-        auto convert = [&](int64_t j) -> bool {
+        auto convert = [&](int64_t j, float& xn) -> bool {
             const int s = (int)(j % XS);
             mbar_wait(su32(&S.xfull[s]), (uint32_t)((j / XS) & 1));
             uint32_t hw[DM / 2], lw[DM / 2];
-            float vmax = 0.f;
+            float vmax = 0.f, n2 = 0.f;
 #pragma unroll
             for (int f = 0; f < DM; f += 2) {
                 const float v0 = (float)fma(S.xd[s][f * TM + p], xs, ncx.v[f]);
                 const float v1 = (float)fma(S.xd[s][(f + 1) * TM + p], xs, ncx.v[f + 1]);
                 vmax = fmaxf(vmax, fmaxf(fabsf(v0), fabsf(v1)));
+                n2 = fmaf(v0, v0, fmaf(v1, v1, n2));
                 const uint32_t h = pack_h2(v0, v1);
                 const float2 hf = __half22float2(u2h(h));
                 hw[f / 2] = h;
@@ -157,9 +185,39 @@ __global__ void __launch_bounds__(NTHR, 1) k_score_mma(const __grid_constant__ C
             tc_fence_before();
             __syncwarp();
             if (lane == 0) arrive(&S.aeready[w]);  // per warp: its 32 events are staged
+            xn = sqrt_approx(n2);
             return !(vmax <= 16384.f);
         };
-        bool ovf = w < J ? convert(w) : false, ovf_next = false;
+        bool ovf = w < J ? convert(w, xnorm) : false, ovf_next = false;
+        // weighted quantities (ll, predict, mixture flags) are needed only when requested:
+        // detect (best component, its density, the flag) refines the unweighted argmax alone
+        const bool need_w = o.ll != nullptr || o.predict != nullptr || o.mode == 1 || o.sum_ll;
+        // FP64 log N(x_e | k) of an event of this warpgroup's tile (planar FP64 tile, stage s):
+        // z = W_k (x - mu_k) as a sum of columns (16 independent accumulators)
+        auto refine = [&](int s, int e, int k) -> double {
+            const double* WTk = S.W64 + k * W64S;  // column f of W_k at WTk[f * DM + r]
+            const double* mk = S.mu64 + k * (DM + 2);
+            double z[DM];
+#pragma unroll
+            for (int r = 0; r < DM; ++r) z[r] = 0.0;
+#pragma unroll
+            for (int f = 0; f < DM; ++f) {
+                const double df = S.xd[s][f * TM + e] - mk[f];
+#pragma unroll
+                for (int r = f & ~1; r < DM; r += 2) {  // W is lower triangular: rows r >= f
+                    const double2 wv = *reinterpret_cast<const double2*>(WTk + f * DM + r);
+                    z[r] = fma(wv.x, df, z[r]);
+                    z[r + 1] = fma(wv.y, df, z[r + 1]);
+                }
+            }
+            double q0 = 0.0, q1 = 0.0;
+#pragma unroll
+            for (int r = 0; r < DM; r += 2) {
+                q0 = fma(z[r], z[r], q0);
+                q1 = fma(z[r + 1], z[r + 1], q1);
+            }
+            return S.ln64[k] - 0.5 * (q0 + q1);
+        };
         int64_t jj = 0;
         for (int64_t j = w; j < J; j += NWG, ++jj) {
             const int s = (int)(j % XS);
@@ -167,130 +225,156 @@ __global__ void __launch_bounds__(NTHR, 1) k_score_mma(const __grid_constant__ C
             const bool valid = i < n;
             mbar_wait(su32(&S.edone[w]), (uint32_t)(jj & 1));
             tc_fence_after();
-            float wk[KMAX], ln[KMAX];
+            // FP32 densities of all K and a per-(event, component) bound dw on their error.
+            // U^ = U / t_k from 4 kind::f16 dispatches: b^ (fp32, exact in the accumulator), then
+            // x_hi B_hi, x_hi B_lo, x_lo B_hi with x^ = x_hi + x_lo, B = B_hi + B_lo (fp16).  Per
+            // entry a:  |U^_a - U_a| <= eps1' sum_f |B_af| |x^_f| + eps2' |b^_a| + eps3 |U^_a|,
+            // eps1' <= 2^-24 (x^ rounding) + 3 2^-22 (split residuals, dropped lo*lo) + 2^-23
+            // (accumulator truncation against the products), eps2' <= 2^-24 (fp32(b^)) + 2^-23
+            // (truncation against the accumulator input), eps3 = 3 2^-23 (truncation of the three
+            // later dispatches, measured ~1 ulp of the running sum, scripts/umma_probe.cu); doubled
+            // here: eps1 = 2^-19, eps2 = 2^-22, eps3 = 2^-21.  Cauchy-Schwarz over a gives
+            //   ||dU|| <= e = eps1 ||B_k||_F ||x^|| + eps2 ||b^_k|| + eps3 ||U^||,
+            //   |q^ - q| <= 2 ||U^|| e + e^2 + 2^-20 q^ (FP32 sum of 16 squares),
+            //   |w^ - w| <= hq (|q^ - q|) + 2^-21 (|w^| + |cst| + 1)   (hq = t_k^2 / 2).
+            float wk[KMAX], dw[KMAX];  // ln_k = wk_k - (cst_k - lnf_k), recomputed where needed
             float m = -INFINITY, bl = -INFINITY;
+            int km = 0, kb = 0;
 #pragma unroll
-            for (int k = 0; k < KMAX; ++k) {
-                float u[16];
-                tmem_ld16(tmem + lq + 16 * k, u);
+            for (int k0 = 0; k0 < KMAX; k0 += 2) {  // two components per TMEM wait
+                float u[2][16];
+                tmem_ld16(tmem + lq + 16 * k0, u[0]);
+                tmem_ld16(tmem + lq + 16 * (k0 + 1), u[1]);
                 tmem_wait_ld();
-                uint64_t q2 = 0;
-#pragma unroll
-                for (int r = 0; r < 16; r += 2) {
-                    const uint64_t uu = pack2(u[r], u[r + 1]);
-                    ffma2(q2, uu, uu);
+                if (k0 + 2 == KMAX) {  // the accumulator is free for the next E-step
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) arrive(&S.efree);
                 }
-                float qa, qb;
-                unpack2(q2, qa, qb);
-                const float hqq = hq[k] * (qa + qb);
-                ln[k] = lnf[k] - hqq;
-                wk[k] = cst[k] - hqq;
-                m = fmaxf(m, wk[k]);
-                bl = fmaxf(bl, ln[k]);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int k = k0 + h;
+                    uint64_t qa2 = 0, qb2 = 0;  // two independent FFMA2 chains
+#pragma unroll
+                    for (int r = 0; r < 16; r += 4) {
+                        const uint64_t ua = pack2(u[h][r], u[h][r + 1]), ub = pack2(u[h][r + 2], u[h][r + 3]);
+                        ffma2(qa2, ua, ua);
+                        ffma2(qb2, ub, ub);
+                    }
+                    float a0, a1, b0, b1;
+                    unpack2(qa2, a0, a1);
+                    unpack2(qb2, b0, b1);
+                    const float q = (a0 + a1) + (b0 + b1);
+                    const float hqq = hq[k] * q;
+                    const float lnk = lnf[k] - hqq;
+                    wk[k] = cst[k] - hqq;
+                    const float rr = sqrt_approx(q);
+                    const float e = fmaf(S.ec1[k], xnorm, fmaf(0x1p-21f, rr, S.ec0[k]));
+                    const float dq = fmaf(rr, fmaf(2.f, e, 0x1p-20f * rr), e * e);
+                    dw[k] = fmaf(hq[k], dq, 0x1p-21f * (fabsf(wk[k]) + fabsf(cst[k]) + 1.f));
+                    if (k < K && wk[k] > m) {  // ties -> lowest k
+                        m = wk[k];
+                        km = k;
+                    }
+                    if (k < K && lnk > bl) {
+                        bl = lnk;
+                        kb = k;
+                    }
+                }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) arrive(&S.efree);
             // E(j) has consumed this WG's A operand: stage the next tile now
-            if (j + NWG < J) ovf_next = convert(j + NWG);
-            // candidates needing FP64: responsibility above 1e-6 (FP32 error then moves ll by
-            // < 1e-6 * 1e-3 relative), or within FP32 rounding of either argmax / of log delta
-            unsigned cand = 0;
+            if (j + NWG < J) ovf_next = convert(j + NWG, xnorm_next);
+            // FP64 recomputation: the unweighted argmax kb (best_k, best_logdens, the flag) by
+            // every thread for its own event; as "extra" pairs every component whose bound
+            // interval reaches kb's, and, when weighted outputs are requested, the weighted
+            // argmax, its contenders and every component with gamma_k dw_k > tau / 8 (the
+            // others enter ll = LSE_k w_k with their FP32 value: ll error <= tau + the FP32 LSE
+            // rounding).  ovf: every component.
+            const float tau8 = 2.5e-8f * fmaxf(1.f, fabsf(m) - 2.1f);
+            const float dm = dw[km], db = dw[kb];
+            unsigned extra = 0;
 #pragma unroll
             for (int k = 0; k < KMAX; ++k) {
-                const float tol = 1e-3f * (1.f + fabsf(wk[k]));
-                bool c;
-                if (refine_all)
-                    c = wk[k] >= m - 13.9f || ln[k] >= bl - tol;
-                else
-                    c = wk[k] >= m - tol || ln[k] >= bl - tol ||
-                        (ln[k] == bl && fabsf(bl - ldf) <= 1e-3f * (1.f + fabsf(ldf)));
-                if (valid && k < K && (c || ovf)) cand |= 1u << k;
-            }
-            // component-major compaction inside the warp (fixed order: component, lane); each
-            // component segment padded to an even length (two events of one component per item).
-            // Warp-local: no warpgroup barrier, each warp refines its own 32 events.
-            uint8_t* cev = S.cev[w] + q * (KMAX * 32 + KMAX);
-            uint8_t* ccomp = S.ccomp[w] + q * (KMAX * 32 + KMAX);
-            int nc = 0;
-#pragma unroll
-            for (int k = 0; k < KMAX; ++k) {
-                const unsigned kb = __ballot_sync(0xffffffffu, (cand >> k) & 1u);
-                if ((cand >> k) & 1u) {
-                    const int pos = nc + __popc(kb & lt_mask);
-                    cev[pos] = (uint8_t)p;
-                    ccomp[pos] = (uint8_t)k;
+                const float lnk = wk[k] - (cst[k] - lnf[k]);
+                bool c = lnk + dw[k] >= bl - db;
+                if (need_w) {
+                    if (refine_all == 1)  // ES_SCORE_REFINE=all: every component with gamma > 1e-6
+                        c = c || wk[k] >= m - 13.9f;
+                    else
+                        c = c || k == km || wk[k] + dw[k] >= m - dm ||
+                            ex2((wk[k] - m) * 1.4426950408889634f) * dw[k] > tau8;
                 }
-                nc += __popc(kb);
-                if (nc & 1) {
-                    if (lane == 0) {
-                        cev[nc] = 0xFFu;
-                        ccomp[nc] = (uint8_t)k;
-                    }
-                    ++nc;
-                }
+                if (refine_all == 3) c = false;  // diagnostics: no FP64 pass at all
+                if (valid && k < K && k != kb && (c || ovf)) extra |= 1u << k;
             }
-            __syncwarp();
-            // FP64 refinement, two events of one component per lane (each W row load serves both)
+#ifdef ES_SCORE_COUNT
+            if (valid) atomicAdd(&g_score_pairs, (unsigned long long)(1 + __popc(extra)));
+#endif
+            const double lp = (valid && refine_all != 3) ? refine(s, p, kb) : (double)(wk[kb] - (cst[kb] - lnf[kb]));
+            // extra pairs: compacted per warp (lane order, then component), one pair per lane
             double* lnv = S.lnv[w];
-            for (int pidx = 2 * lane; pidx < nc; pidx += 64) {
-                const int k = ccomp[pidx];
-                const int e0 = cev[pidx], e1r = cev[pidx + 1];
-                const int e1 = e1r == 0xFF ? e0 : e1r;
-                const double* WTk = S.W64 + k * W64S;  // column f of W_k at WTk[f * DM + r]
-                const double* mk = S.mu64 + k * (DM + 2);
-                // z = W_k (x - mu_k) as a sum of columns: 16 independent accumulators per event
-                double z0[DM], z1[DM];
+            const unsigned any = __ballot_sync(0xffffffffu, extra != 0);
+            if (any) {
+                const int cnt = __popc(extra);
+                int off = cnt;  // inclusive prefix over lanes
 #pragma unroll
-                for (int r = 0; r < DM; ++r) z0[r] = z1[r] = 0.0;
-#pragma unroll
-                for (int f = 0; f < DM; ++f) {
-                    const double df0 = S.xd[s][f * TM + e0] - mk[f];
-                    const double df1 = S.xd[s][f * TM + e1] - mk[f];
-#pragma unroll
-                    for (int r = f & ~1; r < DM; r += 2) {  // W is lower triangular: rows r >= f
-                        const double2 wv = *reinterpret_cast<const double2*>(WTk + f * DM + r);
-                        z0[r] = fma(wv.x, df0, z0[r]);
-                        z1[r] = fma(wv.x, df1, z1[r]);
-                        z0[r + 1] = fma(wv.y, df0, z0[r + 1]);
-                        z1[r + 1] = fma(wv.y, df1, z1[r + 1]);
-                    }
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, off, d);
+                    if (lane >= d) off += v;
                 }
-                double q0 = 0.0, q1 = 0.0;
-#pragma unroll
-                for (int r = 0; r < DM; ++r) {
-                    q0 = fma(z0[r], z0[r], q0);
-                    q1 = fma(z1[r], z1[r], q1);
+                const int tot = __shfl_sync(0xffffffffu, off, 31);
+                off -= cnt;
+                uint16_t* lst = S.plist[w] + q * 256;
+                for (unsigned b = extra; b; b &= b - 1) lst[off++] = (uint16_t)((p << 4) | (__ffs(b) - 1));
+                __syncwarp();
+                for (int pi = lane; pi < tot; pi += 32) {
+                    const int pe = lst[pi];
+                    lnv[(pe & 15) * TM + (pe >> 4)] = refine(s, pe >> 4, pe & 15);
                 }
-                lnv[k * TM + e0] = S.ln64[k] - 0.5 * q0;
-                if (e1r != 0xFF) lnv[k * TM + e1] = S.ln64[k] - 0.5 * q1;
+                __syncwarp();
             }
-            __syncwarp();
             if (lane == 0) arrive(&S.xfree[s]);  // this warp no longer reads the FP64 tile
-            double mm = -INFINITY, bb = -INFINITY;
-            int am = 0, ab = 0;
-            double w64[KMAX];
-#pragma unroll
-            for (int k = 0; k < KMAX; ++k) {
-                const double l = ((cand >> k) & 1u) ? lnv[k * TM + p] : (double)ln[k];
-                w64[k] = S.lp64[k] + l;
-                if (k >= K) continue;
-                if (w64[k] > mm) {
-                    mm = w64[k];
-                    am = k;
-                }
-                if (l > bb) {
+            // best component (ties -> lowest k) among the refined ones; non-refined components
+            // lie below kb's bound interval
+            double bb = lp;
+            int ab = kb;
+            for (unsigned b = extra; b; b &= b - 1) {
+                const int k = __ffs(b) - 1;
+                const double l = lnv[k * TM + p];
+                if (l > bb || (l == bb && k < ab)) {
                     bb = l;
                     ab = k;
                 }
             }
-            // log-sum-exp about the FP64 maximum: the max term is exactly 1, the others are
-            // summed with FP32 exp (relative 1e-7 of a sum >= 1 -> ll error < 2e-7 absolute)
-            float ss = 0.f;
+            double lld = 0.0;
+            int am = 0;
+            if (need_w) {
+                double mm = -INFINITY;
+                double w64[KMAX];
 #pragma unroll
-            for (int k = 0; k < KMAX; ++k)
-                if (k < K) ss += __expf((float)(w64[k] - mm));
-            const double lld = mm + log((double)ss);
+                for (int k = 0; k < KMAX; ++k) {
+                    double l;
+                    if (k == kb)
+                        l = lp;
+                    else if ((extra >> k) & 1u)
+                        l = lnv[k * TM + p];
+                    else
+                        l = (double)(wk[k] - (cst[k] - lnf[k]));
+                    w64[k] = S.lp64[k] + l;
+                    if (k < K && w64[k] > mm) {
+                        mm = w64[k];
+                        am = k;
+                    }
+                }
+                // log-sum-exp about the FP64 maximum: the max term is exactly 1, the others are
+                // ex2.approx terms (relative error ~2^-22.5 each of a sum in [1, K]); logf is
+                // correctly rounded to 1 ulp of a result in [0, log K]: ll error < 4e-7 absolute
+                float ss = 0.f;
+#pragma unroll
+                for (int k = 0; k < KMAX; ++k)
+                    if (k < K) ss += ex2((float)(w64[k] - mm) * 1.4426950408889634f);
+                lld = mm + (double)logf(ss);
+            }
             if (valid) {
                 ll_acc += lld;
                 const uint8_t f = ((o.mode == 1) ? lld : bb) < o.log_delta ? 1 : 0;
@@ -302,6 +386,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_score_mma(const __grid_constant__ C
                 if (o.flags) o.flags[i] = f;
             }
             ovf = ovf_next;
+            xnorm = xnorm_next;
         }
         // per-CTA [sum ll, flag count], fixed-order reduction over the 8 warps
         const double a1 = warp_sum(ll_acc), a2 = warp_sum(nflag);
@@ -380,10 +465,21 @@ void launch_score_mma(const CUtensorMap* xmap, int64_t n, int D, int K, const do
     static int refine_all = -1;
     if (refine_all < 0) {
         const char* e = getenv("ES_SCORE_REFINE");
-        refine_all = (e && e[0] == 'm') ? 0 : 1;  // ES_SCORE_REFINE=min: decisive components only
+        // ES_SCORE_REFINE=all: every component with gamma > 1e-6; =argmax / =none: diagnostics
+        refine_all = !e ? 0 : e[0] == 'a' && e[1] == 'l' ? 1 : e[0] == 'a' ? 2 : e[0] == 'n' ? 3 : 0;
     }
     k_score_mma<<<grid, NTHR, smem, s>>>(*xmap, n, D, K, model, center, xs, ncx, o, blocksum, refine_all);
     ++ls.launches;
 }
 
 }  // namespace es
+
+#ifdef ES_SCORE_COUNT
+extern "C" unsigned long long es_debug_score_pairs(void) {
+    unsigned long long v = 0;
+    cudaMemcpyFromSymbol(&v, es::g_score_pairs, sizeof(v));
+    unsigned long long z = 0;
+    cudaMemcpyToSymbol(es::g_score_pairs, &z, sizeof(z));
+    return v;
+}
+#endif

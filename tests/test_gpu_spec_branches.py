@@ -119,12 +119,12 @@ def test_select_k_bic_spec_examples_full_covariance(es, oracle):
     best, bic = es.select_k_bic(blob, [1, 2, 3], init="kmeans++", seed=3)
     ob, obic = oracle.select_k_bic(blob, [1, 2, 3], init="kmeans++", seed=3)
     assert best == ob == 1
-    assert np.allclose(bic, obic, rtol=1e-9, atol=0)
+    assert np.allclose(bic, obic, rtol=LL_TOL, atol=0)
     two = np.concatenate([rng.normal(-10, 1, size=(300, 2)), rng.normal(10, 1, size=(300, 2))])
     best, bic = es.select_k_bic(two, [1, 2, 3], init="kmeans++", seed=3)
     ob, obic = oracle.select_k_bic(two, [1, 2, 3], init="kmeans++", seed=3)
     assert best == ob == 2
-    assert np.allclose(bic, obic, rtol=1e-9, atol=0)
+    assert np.allclose(bic, obic, rtol=LL_TOL, atol=0)
     best, bic = es.select_k_bic(two, [1], seed=3)
     assert best == 1 and len(bic) == 1
 
