@@ -230,6 +230,7 @@ def run_ours(args):
     barrier(world)
     em_ms_max = max_over_ranks(em_ms, world)
     npass = em.record_passes
+    last_kernel = em.last_kernel
     model = em.finish()
     em.close()
 
@@ -238,9 +239,10 @@ def run_ours(args):
     flags = torch.empty(n_loc, dtype=torch.uint8, device="cuda")
     bk = torch.empty(n_loc, dtype=torch.int32, device="cuda")
     bl = torch.empty(n_loc, dtype=torch.float64, device="cuda")
+    idx = torch.empty(max(n_loc, 1), dtype=torch.int64, device="cuda")  # anomaly indices stay in HBM
     d, ld = es.calibrate_threshold(model, ds, 0.01, n_train=n_global // 2, return_log=True)
     for _ in range(max(args.warmup, 1)):
-        es.detect(model, ds, log_delta=ld, flags=flags, best_k=bk, best_logdens=bl, indices=True)
+        es.detect(model, ds, log_delta=ld, flags=flags, best_k=bk, best_logdens=bl, indices=idx)
     barrier(world)
     torch.cuda.synchronize()
     lib.es_ctx_set_timing(ctx.handle, 1)
@@ -249,7 +251,7 @@ def run_ours(args):
     s0.record(stream)
     nflag = 0
     for _ in range(args.steps):
-        r = es.detect(model, ds, log_delta=ld, flags=flags, best_k=bk, best_logdens=bl, indices=True)
+        r = es.detect(model, ds, log_delta=ld, flags=flags, best_k=bk, best_logdens=bl, indices=idx)
         nflag = r.n_flagged
     s1.record(stream)
     torch.cuda.synchronize()
@@ -289,19 +291,11 @@ def run_ours(args):
     if rank != 0:
         return
     hbm, src = peaks()
-    ek = os.environ.get("ES_EM_KERNEL", "mma")
-    em_kernel = (f"k_em_mma<{npass}> (tcgen05: 3xfp16 E-step whitening + block-diagonal Gram of fp16 "
-                 f"{'hi+lo ' if npass == 2 else ''}records, FP64 flush)"
-                 if ctx.precision == "mixed" and ek.startswith("m") else
-                 "k_em_ws (warp-specialized: TMA + tcgen05 3xTF32 whitening | FP32/FP64 M-step warps)"
-                 if ctx.precision == "mixed" and ek.startswith("w") else
-                 "k_em_tc (tcgen05 3xTF32 whitening + FP32/FP64 M-step)" if ctx.precision == "mixed" and ek == "tc" else
-                 "k_em_fast<16> (SIMT FP32)" if ctx.precision == "mixed" else "k_em_team<16,2> (FP64)")
-    sk = os.environ.get("ES_SCORE_KERNEL", "mma")
-    sc_kernel = ("k_score_mma (tcgen05 3xfp16 whitening + FP64 candidate refinement, 3 warpgroups)"
-                 if ctx.precision == "mixed" and sk.startswith("m") else
-                 "k_score_tc (tcgen05 3xTF32 + FP64 candidate refine)" if ctx.precision == "mixed" and sk == "tc" else
-                 "k_score_fast<16> (FP32 + FP64 refine)" if ctx.precision == "mixed" else "k_score_team<16> (FP64)")
+    em_kernel = (f"{last_kernel} (tcgen05: 3xfp16 E-step whitening + block-diagonal Gram of fp16 "
+                 f"{'hi+lo ' if npass == 2 else ''}records, FP64 flush)" if last_kernel.startswith("k_em_mma")
+                 else last_kernel)
+    sc_kernel = ("k_score_mma (tcgen05 3xfp16 whitening, proven FP32 error bound, FP64 recomputation of the "
+                 "best component, 3 warpgroups)" if ctx.precision == "mixed" else "k_score_team<16> (FP64)")
     it_s = args.steps / (em_ms_max / 1e3)
     bytes_iter = n_global * D * 8
     em_kern_avg = kern_ms / max(kern_n, 1)
@@ -338,6 +332,18 @@ def run_ours(args):
     print(json.dumps(line))
 
 
+def spawn_ranks(n_gpus):
+    """`--gpus N` without a launcher: re-run this command as N ranks (one process per GPU)
+    under torch.distributed.run on 127.0.0.1; rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n_gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -352,6 +358,10 @@ def main():
     ap.add_argument("--traffic-note", default="dram__bytes_read.sum + dram__bytes_write.sum of k_em_mma<1> at N=2^26, "
                                               "profiles/r01_k_em_mma1_ncu_summary.txt")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args.gpus)
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} disagrees with WORLD_SIZE={os.environ['WORLD_SIZE']}")
     if args.impl == "reference":
         run_reference(args)
     else:

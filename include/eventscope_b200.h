@@ -164,6 +164,9 @@ int es_gmm_em_free(es_em_state* st);
 /* Record precision of the last fused (tcgen05) E+M pass: 1 = single fp16 record
  * (every component had >= 2^20 events), 2 = fp16 hi + lo records, 0 = another kernel. */
 int es_gmm_em_record_passes(const es_em_state* st, int32_t* passes);
+/* Name of the EM pass kernel the last iteration ran ("k_em_mma<1>", "k_em_diag_mixed",
+ * "strict FP64 (...)", ...; static storage). */
+int es_gmm_em_last_kernel(const es_em_state* st, const char** name);
 
 /* ------------------------------------------------------------- score ---- */
 /* Per local event (any output nullable): ll = log p(x); predict = argmax

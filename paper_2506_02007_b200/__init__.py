@@ -105,6 +105,19 @@ def _check(status: int) -> None:
                               lib.es_last_error_message().decode())
 
 
+def _check_tensor(t, dtype: str, ndim: int) -> None:
+    """A torch tensor handed to the library: its dtype must be what the C-ABI reads (no silent
+    reinterpretation) and, on the GPU, the work that produced it must be complete - the library
+    reads it on its own streams, so the caller's current stream is synchronised first."""
+    if str(t.dtype).replace("torch.", "") != dtype:
+        raise EventscopeError("Data", "InvalidDtype", f"expected a {dtype} tensor, got {t.dtype}")
+    if t.dim() != ndim:
+        raise EventscopeError("Data", "DimensionMismatch", f"expected a {ndim}-D tensor, got {t.dim()}-D")
+    if t.is_cuda:
+        import torch
+        torch.cuda.current_stream(t.device).synchronize()
+
+
 def _ptr(a) -> Optional[int]:
     """Address of a numpy array or torch tensor (host or device); None passes NULL."""
     if a is None:
@@ -186,6 +199,8 @@ class Context:
             _check(lib.es_ctx_create(device, C.byref(h)))
         self.handle = h
         self.device, self.rank, self.world = device, rank, world
+        import weakref
+        self._datasets = weakref.WeakSet()
         self.set_precision(os.environ.get("ES_PRECISION", precision))
 
     def set_precision(self, mode: str) -> None:
@@ -220,6 +235,8 @@ class Context:
 
     def close(self) -> None:
         if getattr(self, "handle", None):
+            for ds in list(getattr(self, "_datasets", ())):  # datasets first (the library detaches any left)
+                ds.close()
             self._lib.es_ctx_destroy(self.handle)
             self.handle = None
 
@@ -246,6 +263,8 @@ class Dataset:
     def __init__(self, ctx: Context, handle: C.c_void_p):
         self.ctx = ctx
         self.handle = handle
+        if hasattr(ctx, "_datasets"):
+            ctx._datasets.add(self)
         nl, ng, off, d = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int32()
         _check(ctx._lib.es_dataset_info(handle, C.byref(nl), C.byref(ng), C.byref(off), C.byref(d)))
         self.n_local, self.n_global, self.row_offset, self.D = nl.value, ng.value, off.value, d.value
@@ -255,6 +274,7 @@ class Dataset:
         """X: numpy (N,D) float64 (any strides) or a CUDA torch tensor (row- or column-major)."""
         ctx = ctx or default_context()
         if hasattr(X, "data_ptr"):
+            _check_tensor(X, "float64", 2)
             n, d = X.shape
             rs, cs = X.stride()
             ptr = X.data_ptr()
@@ -309,12 +329,20 @@ def _as_dataset(X, ctx: Optional[Context]) -> Dataset:
     return X if isinstance(X, Dataset) else Dataset.from_array(X, ctx)
 
 
+def _seed(seed: Optional[int]) -> int:
+    """An explicit seed wins; an omitted one (None) takes EACGM_SEED (the CLI-level
+    override) or 0.  Applied identically by every seeded entry point (fits, BIC, pipeline,
+    k-means baseline)."""
+    if seed is not None:
+        return int(seed)
+    env = os.environ.get("EACGM_SEED")
+    return int(env) if env is not None else 0
+
+
 def _opts(init, tol, max_iter, reg, seed, covariance_type="full") -> _FitOpts:
     code = {"random": ES_INIT_RANDOM, "kmeans++": ES_INIT_KMEANSPP, "kmeanspp": ES_INIT_KMEANSPP,
             "given": ES_INIT_GIVEN}[init] if isinstance(init, str) else int(init)
-    env = os.environ.get("EACGM_SEED")  # SPEC.md:529
-    if env is not None:
-        seed = int(env)
+    seed = _seed(seed)
     return _FitOpts(code, float(tol), int(max_iter), -1.0 if reg is None else float(reg), int(seed),
                     {"full": 0, "diag": 1}[covariance_type])
 
@@ -322,7 +350,7 @@ def _opts(init, tol, max_iter, reg, seed, covariance_type="full") -> _FitOpts:
 class EM:
     """Stepwise EM engine (es_gmm_em_begin/step/end): same semantics as fit_em."""
 
-    def __init__(self, X, K: int, init="kmeans++", tol=1e-6, max_iter=200, reg=None, seed=0,
+    def __init__(self, X, K: int, init="kmeans++", tol=1e-6, max_iter=200, reg=None, seed=None,
                  init_params: Optional[GmmModel] = None, ctx: Optional[Context] = None, covariance_type="full"):
         self.ds = _as_dataset(X, ctx)
         self.ctx = self.ds.ctx
@@ -354,6 +382,13 @@ class EM:
         v = C.c_int32()
         _check(self.ctx._lib.es_gmm_em_record_passes(self.handle, C.byref(v)))
         return v.value
+    @property
+    def last_kernel(self) -> str:
+        """EM pass kernel of the last iteration (e.g. 'k_em_mma<1>', 'k_em_diag_mixed')."""
+        v = C.c_char_p()
+        _check(self.ctx._lib.es_gmm_em_last_kernel(self.handle, C.byref(v)))
+        return v.value.decode()
+
     def finish(self) -> GmmModel:
         K, D = self.K, self.ds.D
         w, m, c = np.empty(K), np.empty((K, D)), np.empty((K, D, D))
@@ -378,7 +413,7 @@ class EM:
 
 
 def fit_em(X, K: int, init="kmeans++", tol: float = 1e-6, max_iter: int = 200, reg: Optional[float] = None,
-           seed: int = 0, init_params: Optional[GmmModel] = None, ctx: Optional[Context] = None,
+           seed: Optional[int] = None, init_params: Optional[GmmModel] = None, ctx: Optional[Context] = None,
            covariance_type: str = "full") -> GmmModel:
     """EM fit.  Defaults per SPEC.md:319-321.  covariance_type "diag" is an
     extension (diagonal covariances, not in the reference)."""
@@ -498,7 +533,7 @@ def calibrate_threshold(model: GmmModel, X_train, q: float, mode: str = "compone
     return (d.value, ld.value) if return_log else d.value
 
 
-def select_k_bic(X, k_range: Sequence[int], init="kmeans++", tol=1e-6, max_iter=200, reg=None, seed=0,
+def select_k_bic(X, k_range: Sequence[int], init="kmeans++", tol=1e-6, max_iter=200, reg=None, seed=None,
                  ctx: Optional[Context] = None, covariance_type: str = "full"):
     """(best_K, bic_values); failed K -> NaN."""
     ds = _as_dataset(X, ctx)
@@ -526,7 +561,8 @@ class PipelineResult:
 
 def run_pipeline(X, K: int, train_window: float = 0.5, quantile_q: Optional[float] = 0.01,
                  delta: Optional[float] = None, standardize: bool = True, mode: str = "component",
-                 init="kmeans++", tol: float = 1e-6, max_iter: int = 200, reg: Optional[float] = None, seed: int = 0,
+                 init="kmeans++", tol: float = 1e-6, max_iter: int = 200, reg: Optional[float] = None,
+                 seed: Optional[int] = None,
                  ctx: Optional[Context] = None) -> PipelineResult:
     """run_pipeline over a time-ordered feature matrix: fit on the standardized
     first train_window fraction, calibrate delta as the quantile_q-quantile there (or use delta),
@@ -569,7 +605,8 @@ class KMeansResult:
     iterations: int
 
 
-def kmeans_baseline(X, K: int, q: float = 0.01, train_window: float = 0.5, seed: int = 0, max_iter: int = 100,
+def kmeans_baseline(X, K: int, q: float = 0.01, train_window: float = 0.5, seed: Optional[int] = None,
+                    max_iter: int = 100,
                     ctx: Optional[Context] = None) -> KMeansResult:
     """KMeans baseline on the device (es_kmeans_baseline): k-means++ seeding and Lloyd's
     algorithm on the first train_window fraction of the events; flag iff the distance to
@@ -580,7 +617,7 @@ def kmeans_baseline(X, K: int, q: float = 0.01, train_window: float = 0.5, seed:
     fl, sc = np.empty(n, np.uint8), np.empty(n)
     thr, nf, it = C.c_double(), C.c_int64(), C.c_int32()
     _check(ds.ctx._lib.es_kmeans_baseline(ds.ctx.handle, ds.handle, C.c_int32(K), C.c_double(q),
-                                          C.c_double(train_window), C.c_uint64(seed), C.c_int32(max_iter),
+                                          C.c_double(train_window), C.c_uint64(_seed(seed)), C.c_int32(max_iter),
                                           C.c_void_p(cen.ctypes.data), C.byref(thr), C.c_void_p(_ptr(fl)),
                                           C.c_void_p(_ptr(sc)), C.byref(nf), C.byref(it)))
     return KMeansResult(cen, thr.value, fl, sc, nf.value, it.value)
@@ -602,6 +639,9 @@ def confusion(labels, flags, ctx: Optional[Context] = None) -> ConfusionMatrix:
     nl, nf = len(labels), len(flags)
     if nl != nf:
         raise EventscopeError("Data", "LengthMismatch", f"labels ({nl}) and flags ({nf}) differ in length")
+    for t in (labels, flags):
+        if hasattr(t, "data_ptr"):
+            _check_tensor(t, "uint8", 1)
     lab = labels if hasattr(labels, "data_ptr") else np.ascontiguousarray(labels, np.uint8)
     fl = flags if hasattr(flags, "data_ptr") else np.ascontiguousarray(flags, np.uint8)
     out = np.zeros(4, np.int64)

@@ -68,7 +68,7 @@ using namespace mma;
 
 // NWG epilogue warpgroups take tiles round robin (2; 3 is an NPASS = 1 option,
 // ES_EM_MMA_WG), then a TMA warp and an MMA-issuer warp.
-constexpr int nthr(int nwg) { return 128 * nwg + 64; }
+constexpr int nthr(int nwg) { return 128 * nwg + 96; }  // + TMA warp, E-issuer warp, Gram-issuer warp
 constexpr uint32_t GRP = (TM / 8) * 128;   // one MN-major group of 8 columns: 16 K-groups x 128 B
 constexpr uint32_t RECL = 16 * GRP;        // 32768 B
 constexpr int MREG0 = 128;                 // two Gram regions (tile parity) from TMEM column 128
@@ -107,10 +107,10 @@ __global__ void __launch_bounds__(nthr(NWG), 1) k_em_mma(const __grid_constant__
                                                           const double* __restrict__ center, double xs,
                                                           const __grid_constant__ NegCx ncx,
                                                           const __grid_constant__ NegCxF ncxf, const float xsf,
-                                                          int policy, double* __restrict__ partial) {
+                                                          double* __restrict__ partial) {
     using Sm = Smem<NPASS, NWG>;
     constexpr int XS = Sm::XS, NTHR = nthr(NWG), MREGS = mregs(NPASS), TA0 = ta0(NPASS), TONE = tone(NPASS, NWG);
-    constexpr int WTMA = 4 * NWG, WMMA = 4 * NWG + 1;
+    constexpr int WTMA = 4 * NWG, WMMA = 4 * NWG + 1, WGRM = 4 * NWG + 2;
     extern __shared__ __align__(128) unsigned char smraw[];
     // keep the shared-window provenance of the pointer (generic LD/ST otherwise)
     Sm& S = *reinterpret_cast<Sm*>(smraw + ((128u - (su32(smraw) & 127u)) & 127u));
@@ -515,7 +515,30 @@ __global__ void __launch_bounds__(nthr(NWG), 1) k_em_mma(const __grid_constant__
             }
         }
     } else if (warp == WMMA) {
-        // ========================================================== MMA issuer
+        // ==================================================== E-step MMA issuer
+        // Two issuer warps (E-steps, Grams), each blocked on its mbarriers with a suspend
+        // hint: no polling loop takes issue slots from the epilogue warps of its SM
+        // sub-partition (a polling single issuer was ~7% of the kernel's instructions).
+        if (lane == 0) {
+            const uint64_t dbh = sdesc(su32(S.bw[0]), 128, 256), dbl = sdesc(su32(S.bw[1]), 128, 256);
+            const uint64_t dbb = sdesc(su32(S.bb), 128, 256);
+            for (int64_t je = 0; je < J; ++je) {
+                const int w = (int)(je % NWG);
+                mbar_wait_sleep(su32(&S.aeready[w]), (uint32_t)((je / NWG) & 1));
+                if (je >= 1) mbar_wait_sleep(su32(&S.efree), (uint32_t)((je - 1) & 1));
+                TRACE(1, je);
+                tc_fence_after();
+                const uint32_t tah = tmem + TA0 + 16 * w, tal = tah + 8;
+                mma_f16_ta(tmem, tmem + TONE, dbb, kIdescE, 0u);  // fp32(b') exactly, first
+                mma_f16_ta(tmem, tah, dbh, kIdescE, 1u);
+                mma_f16_ta(tmem, tah, dbl, kIdescE, 1u);
+                mma_f16_ta(tmem, tal, dbh, kIdescE, 1u);
+                commit(&S.edone[w]);
+                TRACE(9, je);
+            }
+        }
+    } else if (warp == WGRM) {
+        // ======================================================= Gram MMA issuer
         if (lane == 0) {
             constexpr uint32_t idesc1 = idesc_f16(128, NPASS == 2 ? 144 : 136, 1);
             constexpr uint32_t idesc2a = idesc_f16(128, 128, 1);
@@ -530,9 +553,13 @@ __global__ void __launch_bounds__(nthr(NWG), 1) k_em_mma(const __grid_constant__
                 dh0[g] = sdesc(su32(S.rech[g]), 128, GRP);
                 dl0[g] = sdesc(su32(S.recl[NPASS == 2 ? g : 0]), 128, GRP);
             }
-            auto gram = [&](int64_t m) {
-                const int mw = (int)(m % NWG);
-                const uint32_t xg = tmem + (uint32_t)(MREG0 + MREGS * (int)(m & 1));
+            for (int64_t jm = 0; jm < J; ++jm) {
+                const int mw = (int)(jm % NWG);
+                mbar_wait_sleep(su32(&S.mready[mw]), (uint32_t)((jm / NWG) & 1));
+                if (jm >= 2) mbar_wait_sleep(su32(&S.rfree[jm & 1]), (uint32_t)(((jm - 2) >> 1) & 1));
+                TRACE(2, jm);
+                tc_fence_after();
+                const uint32_t xg = tmem + (uint32_t)(MREG0 + MREGS * (int)(jm & 1));
                 const uint64_t dh = mw == 0 ? dh0[0] : (mw == 1 ? dh0[1] : dh0[NWG - 1]);
                 const uint64_t dl = mw == 0 ? dl0[0] : (mw == 1 ? dl0[1] : dl0[NWG - 1]);
 #pragma unroll
@@ -545,47 +572,7 @@ __global__ void __launch_bounds__(nthr(NWG), 1) k_em_mma(const __grid_constant__
                     }
                 }
                 commit(&S.mdone[mw]);
-            };
-            // The tensor pipe runs MMAs in issue order and the issuing thread blocks once a
-            // few are queued, so a Gram issued just before an E-step becomes ready delays the
-            // warpgroups' E -> U read -> E chain.  Policy 0 (default): whichever is ready, E
-            // first.  Policy P > 0: a Gram only right after an E-step, once every E-step is
-            // out, or after P clocks without one (a warpgroup draining its Gram to recentre
-            // waits for it before it releases the next E-step).  Measured (scripts/em_trace.py):
-            // the warpgroups' own per-tile work (~3.4k clocks per warpgroup and tile) is the
-            // critical path, and delaying Grams makes their flushes wait (P = 2000: 4.1 ms
-            // per 2^26-event pass against 3.6 ms).
-            const uint64_t dbh = sdesc(su32(S.bw[0]), 128, 256), dbl = sdesc(su32(S.bw[1]), 128, 256);
-            const uint64_t dbb = sdesc(su32(S.bb), 128, 256);
-            int64_t je = 0, jm = 0;
-            long long tle = clock64();
-            while (jm < J) {
-                bool didE = false;
-                if (je < J && mbar_test(&S.aeready[je % NWG], (uint32_t)((je / NWG) & 1)) &&
-                    (je == 0 || mbar_test(&S.efree, (uint32_t)((je - 1) & 1)))) {
-                    const int w = (int)(je % NWG);
-                    TRACE(1, je);
-                    tc_fence_after();
-                    const uint32_t tah = tmem + TA0 + 16 * w, tal = tah + 8;
-                    mma_f16_ta(tmem, tmem + TONE, dbb, kIdescE, 0u);  // fp32(b') exactly, first
-                    mma_f16_ta(tmem, tah, dbh, kIdescE, 1u);
-                    mma_f16_ta(tmem, tah, dbl, kIdescE, 1u);
-                    mma_f16_ta(tmem, tal, dbh, kIdescE, 1u);
-                    commit(&S.edone[w]);
-                    TRACE(9, je);
-                    ++je;
-                    didE = true;
-                    tle = clock64();
-                }
-                if ((policy == 0 || didE || je == J || clock64() - tle > policy) && jm < je &&
-                    mbar_test(&S.mready[jm % NWG], (uint32_t)((jm / NWG) & 1)) &&
-                    (jm < 2 || mbar_test(&S.rfree[jm & 1], (uint32_t)(((jm - 2) >> 1) & 1)))) {
-                    TRACE(2, jm);
-                    tc_fence_after();
-                    gram(jm);
-                    TRACE(10, jm);
-                    ++jm;
-                }
+                TRACE(10, jm);
             }
         }
     }
@@ -595,11 +582,37 @@ __global__ void __launch_bounds__(nthr(NWG), 1) k_em_mma(const __grid_constant__
     if (warp == WMMA) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// 2-D TMA descriptor over the planar event matrix: dims (rows, planes), box 128 rows x 16
+// planes (the fused passes' FP64 tile), driver entry point resolved through the runtime.
+bool make_event_tmap(CUtensorMap* map, const double* X, int64_t n, int64_t ld, int D) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return false;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    if (n <= 0 || D > 16) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)D};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+    const cuuint32_t box[2] = {TM, (cuuint32_t)D};
+    const cuuint32_t estr[2] = {1, 1};
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(X), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Shapes of the fused tensor-core passes (k_em_mma / k_score_mma): the mixed path's domain.
+bool em_mixed_supported(int D, int K) { return D <= DM && K <= KMAX; }
+
+// ES_EM_KERNEL=fp64 runs the mixed-shape iterations on the strict FP64 kernel instead.
 bool em_mma_enabled() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("ES_EM_KERNEL");
-        v = (!e || e[0] == 'm') ? 1 : 0;  // default; "ws" / "tc" / "simt" select the older kernels
+        v = (e && e[0] == 'f') ? 0 : 1;
     }
     return v == 1;
 }
@@ -610,17 +623,6 @@ int em_mma_passes() {
     if (v < 0) {
         const char* e = getenv("ES_EM_MMA_PASSES");
         v = (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
-    }
-    return v;
-}
-
-// ES_EM_MMA_POLICY: MMA issue policy (0 default: whichever is ready; P > 0: a Gram right
-// after an E-step, or after P clocks without one)
-static int em_mma_policy() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("ES_EM_MMA_POLICY");
-        v = e ? atoi(e) : 0;
     }
     return v;
 }
@@ -638,7 +640,7 @@ static void launch_npass(const CUtensorMap* xmap, int64_t n, int D, int K, const
     NegCxF ncxf{};
     for (int j = 0; j < DM; ++j) ncxf.v[j] = (float)ncx.v[j];
     k_em_mma<NPASS, F32, NWG><<<grid, nthr(NWG), smem, s>>>(*xmap, n, D, K, model, center, xs, ncx, ncxf,
-                                                             (float)xs, em_mma_policy(), partial);
+                                                             (float)xs, partial);
 }
 
 // ES_EM_MMA_WG=3 runs the NPASS = 1 kernel with three epilogue warpgroups (128 registers

@@ -1328,13 +1328,13 @@ __global__ void k_finalize(const double* __restrict__ stats, int G, int D, int K
         for (int e = threadIdx.x; e < D * D; e += blockDim.x) {
             const int a = e / D, b = e % D;
             if (a > b) continue;
-            const double v = (whitened == 2 && a != b) ? 0.0 : sM[a * D + b] + (a == b ? reg : 0.0);
+            const double v = ((whitened == 2 || whitened == 4) && a != b) ? 0.0 : sM[a * D + b] + (a == b ? reg : 0.0);
             sA[a * D + b] = v;
             sA[b * D + a] = v;
         }
         for (int a = threadIdx.x; a < D; a += blockDim.x) {
             double c0 = cold[a];
-            if (whitened == 3) c0 = center[a] + (double)(float)((cold[a] - center[a]) * xs) / xs;
+            if (whitened == 3 || whitened == 4) c0 = center[a] + (double)(float)((cold[a] - center[a]) * xs) / xs;
             sMu[a] = c0 + s1[a] * inv;
         }
     }

@@ -54,13 +54,21 @@ void launch_col_stats(const double* X, int64_t n, int64_t ld, int D, double* scr
 // M-step finalize from G rank blocks of statistics (summed in rank order),
 // updating the model in place and writing IterStatus (+ logL record[t]).
 // whitened: 0 raw statistics, 1 whitened (team kernels), 2 raw + diagonal covariance
-// whitened 3: raw statistics about c + fp32((mu_k - c) xs) / xs (k_em_mma), needs center and xs.
+// whitened 3: raw statistics about c + fp32((mu_k - c) xs) / xs (k_em_mma), needs center and xs;
+// whitened 4: as 3 with diagonal covariances (k_em_diag_mixed, xs = 1).
 void launch_finalize(const double* stats, int G, int D, int K, int64_t n_global, double reg, int whitened,
                      double* model, IterStatus* st, double* record, int t, cudaStream_t s, LaunchStats& ls,
                      const double* center = nullptr, double xs = 1.0);
 // Diagonal-covariance E+M pass (FP64 team kernel, D <= 32, K <= 32).
 void launch_em_diag(const double* X, int64_t n, int64_t ld, int D, int K, const double* model, double* partial,
                     int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
+// Mixed-precision diagonal E+M pass (es_em_diag.cu): FP32 packed arithmetic with per-component
+// centring, FP64 accumulation every 32 events per lane; statistics for finalize mode 4 (diagonal,
+// about center + fp32(mu_k - center)).  D <= 16, K <= 16.
+bool em_diag_mixed_supported(int D, int K);
+void launch_em_diag_mixed(const double* X, int64_t n, int64_t ld, int D, int K, const double* model,
+                          const double* center, double* partial, int num_sms, int* nblk, cudaStream_t s,
+                          LaunchStats& ls);
 // Derive L, W, lognorm, logpi from pi, mu, cov in `model` (all components).
 void launch_derive(double* model, int D, int K, IterStatus* st, cudaStream_t s, LaunchStats& ls);
 // Scoring pass; `blocksum` receives per-CTA [ll_sum, flag_count] pairs.
@@ -82,23 +90,10 @@ void launch_planar_to_rows(const double* X, int64_t ld, int D, int64_t row0, int
 // parts[chunk] = fixed-order sum of d2 over 4096-row chunks.
 void launch_kpp_update(const double* X, int64_t n, int64_t ld, int D, const double* center, double* d2,
                        double* parts, bool first, cudaStream_t s, LaunchStats& ls);
-// Mixed-precision fast path (es_fast.cu): FP32 whitening, FP64 statistics.
-// `center` (D doubles) is subtracted in FP64 before the FP32 conversion.
-bool em_fast_supported(int D, int K);
-void launch_em_fast(const double* X, int64_t n, int64_t ld, int D, int K, const double* model, const double* center,
-                    double* partial, int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
-// tcgen05 E-step variant of the fused pass (D <= 16, K <= 8); ES_EM_KERNEL=simt
-// selects the SIMT FP32 kernel instead.
-bool em_tc_enabled();
-void launch_em_tc(const double* X, int64_t n, int64_t ld, int D, int K, const double* model, const double* center,
-                  double* partial, int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
-// Warp-specialized tcgen05 pass (es_ws.cu), the default (ES_EM_KERNEL=ws|tc|simt).
-bool em_ws_enabled();
-// xmap: 2-D TMA tensor map over the planar event matrix (box = 128 rows x D planes).
-void launch_em_ws(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model, const double* center,
-                  double* partial, int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
-// Fused pass with E-step and M-step Gram on tcgen05 (es_em_mma.cu), the default
-// for D <= 16, K <= 8 (ES_EM_KERNEL=mma|ws|tc|simt).  Writes finalize mode-3 statistics.
+// Shapes of the fused tensor-core passes (D <= 16, K <= 8): the mixed-precision path's domain.
+bool em_mixed_supported(int D, int K);
+// Fused pass with E-step and M-step Gram on tcgen05 (es_em_mma.cu), the mixed-precision EM
+// pass for D <= 16, K <= 8.  Writes finalize mode-3 statistics.
 bool em_mma_enabled();
 // Record precision: npass 2 (fp16 hi + lo records) or 1 (single fp16 record, used when
 // every component has >= kOnePassMinNk events); ES_EM_MMA_PASSES=1|2 overrides.
@@ -114,20 +109,12 @@ void launch_em_mma(const CUtensorMap* xmap, int64_t n, int D, int K, const doubl
                    int* nblk, cudaStream_t s, LaunchStats& ls);
 // Builds that tensor map (driver entry point resolved through the runtime).
 bool make_event_tmap(CUtensorMap* map, const double* X, int64_t n, int64_t ld, int D);
-// tcgen05 scoring pass (es_score_tc.cu); ES_SCORE_KERNEL=simt selects k_score_fast.
-bool score_tc_supported(int D, int K, const ScoreOut& o);
-void launch_score_tc(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model, const double* center,
-                     const ScoreOut& o, double* blocksum, int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
 // Fused-pipeline scoring pass (es_score_mma.cu), the default for D <= 16, K <= 8:
 // center_host / xs as for launch_em_mma (x^ = (x - c) xs, xs a power of two).
 bool score_mma_enabled(int D, int K, const ScoreOut& o);
 void launch_score_mma(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model, const double* center,
                       const double* center_host, double xs, const ScoreOut& o, double* blocksum, int num_sms,
                       int* nblk, cudaStream_t s, LaunchStats& ls);
-bool score_fast_supported(int D, int K, const ScoreOut& o);
-void launch_score_fast(const double* X, int64_t n, int64_t ld, int D, int K, const double* model,
-                       const double* center, const ScoreOut& o, double* blocksum, int num_sms, int* nblk,
-                       cudaStream_t s, LaunchStats& ls);
 // SYN-v1 rows [grow0, grow0+n) written into planar X (local row = global - grow0).
 void launch_synth(double* X, int64_t ld, int64_t n, int64_t grow0, int D, int K, const double* syn_model,
                   uint64_t seed, cudaStream_t s, LaunchStats& ls);

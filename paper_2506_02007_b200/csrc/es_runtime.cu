@@ -176,6 +176,7 @@ struct es_ctx {
     int num_sms = 148;
     LaunchStats ls;
     int64_t collectives = 0;  // NCCL collectives issued (replays of captured ones included)
+    std::vector<es_dataset*> live;  // datasets bound to this context (detached on destroy)
     DevBuf stage2;  // second staging buffer of dataset_create
     // the planes of the last destroyed dataset, kept for the next dataset_create of a
     // similar size (an 8.6 GB cudaMalloc / cudaFree pair per fit-on-fresh-data call is
@@ -308,11 +309,15 @@ struct es_dataset {
 };
 
 es_dataset::~es_dataset() {
+    if (ctx) {
+        auto& v = ctx->live;
+        v.erase(std::remove(v.begin(), v.end(), this), v.end());
+    }
     if (!X) return;
     if (owned_by_cache && ctx)
         ctx->give_planes(X, (size_t)ld * D * 8);
     else
-        cudaFree(X);
+        cudaFree(X);  // also after its context was destroyed (ctx == nullptr): no dangling cache
 }
 
 struct es_em_state {
@@ -327,6 +332,7 @@ struct es_em_state {
     bool f32conv = false;      // max|x| <= 4 max|x - mean|: x^ may be formed on the FP32 pipe
     double min_nk = 0.0;       // min_k N_k of the current model (global), selects k_em_mma's record precision
     int last_npass = 0;        // record precision of the last k_em_mma pass (0: other kernel)
+    int last_path = -1;        // EmIterPath of the last iteration
     DevBuf dcenter;
     SplitMix64 rng{0};
     std::vector<double> per_iter;
@@ -539,10 +545,6 @@ void score_launch(es_ctx* c, const double* X, int64_t n, int64_t ld, int D, int 
     else if (c->precision == 0 && center && center_host && xmap && score_mma_enabled(D, K, o))
         launch_score_mma(xmap, n, D, K, dmodel, center, center_host, xs, o, bs, c->num_sms, nblk, c->stream,
                          c->ls);
-    else if (c->precision == 0 && center && xmap && score_tc_supported(D, K, o))
-        launch_score_tc(xmap, n, D, K, dmodel, center, o, bs, c->num_sms, nblk, c->stream, c->ls);
-    else if (c->precision == 0 && center && score_fast_supported(D, K, o))
-        launch_score_fast(X, n, ld, D, K, dmodel, center, o, bs, c->num_sms, nblk, c->stream, c->ls);
     else
         launch_score(X, n, ld, D, K, dmodel, o, bs, c->num_sms, nblk, c->stream, c->ls);
 }
@@ -760,7 +762,7 @@ void em_begin(es_em_state* st, const es_gmm_params* init) {
 // the per-event rounding of the whitening to average out: below
 // kMixedMinNk events in some component the iteration runs on the strict FP64 kernel.
 bool mixed_em(es_ctx* c, const es_em_state* st) {
-    return c->precision == 0 && em_fast_supported(st->D, st->K) && st->min_nk >= kMixedMinNk;
+    return c->precision == 0 && em_mixed_supported(st->D, st->K) && st->min_nk >= kMixedMinNk;
 }
 
 // logL of the current model from one fused tcgen05 E+M pass (statistics discarded): the
@@ -796,21 +798,22 @@ bool em_logl_pass(es_em_state* st, double* out) {
 }
 
 // Iteration paths (the EM pass kernel and its statistics format).
-enum EmIterPath { kPathEmpty = 0, kPathDiag, kPathStrict, kPathMma1, kPathMma2, kPathWs, kPathTc, kPathFast };
+enum EmIterPath { kPathEmpty = 0, kPathDiag, kPathStrict, kPathMma1, kPathMma2, kPathDiagMixed };
+
+// The mixed diagonal pass needs >= kOnePassMinNk events in every component (its per-event FP32
+// rounding averages out there), the strict FP64 team kernel otherwise.
+bool mixed_diag(const es_ctx* c, const es_em_state* st) {
+    return c->precision == 0 && em_diag_mixed_supported(st->D, st->K) && st->min_nk >= kOnePassMinNk;
+}
 
 int em_choose_path(const es_em_state* st) {
     es_ctx* c = st->ctx;
     const es_dataset* ds = st->ds;
     if (ds->n_local == 0) return kPathEmpty;
-    if (is_diag(st)) return kPathDiag;
-    if (mixed_em(c, st)) {
-        if (em_mma_enabled() && ds->has_xmap) {
-            const int np = em_mma_passes() ? em_mma_passes() : (st->min_nk >= kOnePassMinNk ? 1 : 2);
-            return np == 1 ? kPathMma1 : kPathMma2;
-        }
-        if (em_ws_enabled() && ds->has_xmap) return kPathWs;
-        if (em_tc_enabled()) return kPathTc;
-        return kPathFast;
+    if (is_diag(st)) return mixed_diag(c, st) ? kPathDiagMixed : kPathDiag;
+    if (mixed_em(c, st) && em_mma_enabled() && ds->has_xmap) {
+        const int np = em_mma_passes() ? em_mma_passes() : (st->min_nk >= kOnePassMinNk ? 1 : 2);
+        return np == 1 ? kPathMma1 : kPathMma2;
     }
     return kPathStrict;
 }
@@ -832,31 +835,23 @@ int em_pass_launch(es_em_state* st, int path, int* nblk) {
         case kPathDiag:
             launch_em_diag(ds->X, ds->n_local, ds->ld, D, K, dmodel, part, c->num_sms, nblk, c->stream, c->ls);
             return 2;
+        case kPathDiagMixed:
+            launch_em_diag_mixed(ds->X, ds->n_local, ds->ld, D, K, dmodel, st->dcenter.as<double>(D), part,
+                                 c->num_sms, nblk, c->stream, c->ls);
+            return 4;
         case kPathMma1:
         case kPathMma2:
             launch_em_mma(&ds->xmap, ds->n_local, D, K, dmodel, st->dcenter.as<double>(D), st->mean.data(), st->xs,
                           st->f32conv, path == kPathMma1 ? 1 : 2, part, c->num_sms, nblk, c->stream, c->ls);
             return 3;
-        case kPathWs:
-            launch_em_ws(&ds->xmap, ds->n_local, D, K, dmodel, st->dcenter.as<double>(D), part, c->num_sms, nblk,
-                         c->stream, c->ls);
-            return 0;
-        case kPathTc:
-            launch_em_tc(ds->X, ds->n_local, ds->ld, D, K, dmodel, st->dcenter.as<double>(D), part, c->num_sms,
-                         nblk, c->stream, c->ls);
-            return 0;
-        case kPathFast:
-            launch_em_fast(ds->X, ds->n_local, ds->ld, D, K, dmodel, st->dcenter.as<double>(D), part, c->num_sms,
-                           nblk, c->stream, c->ls);
-            return 0;
         case kPathStrict: {
             bool wh = true;
             launch_em_pass(ds->X, ds->n_local, ds->ld, D, K, dmodel, part, c->num_sms, nblk, &wh, c->stream, c->ls);
             return wh ? 1 : 0;
         }
         default:  // an empty shard announces the statistics format the other ranks use
-            if (is_diag(st)) return 2;
-            if (mixed_em(c, st)) return em_mma_enabled() ? 3 : 0;
+            if (is_diag(st)) return mixed_diag(c, st) ? 4 : 2;
+            if (mixed_em(c, st) && em_mma_enabled()) return 3;
             return em_path(D, K) != EmPath::Generic ? 1 : 0;
     }
 }
@@ -995,6 +990,7 @@ bool em_iterate(es_em_state* st) {
         CU(cudaMemcpyAsync(backup, dmodel, mstride(K, D) * 8, cudaMemcpyDeviceToDevice, c->stream));
     const int path = em_choose_path(st);
     st->last_npass = path == kPathMma1 ? 1 : path == kPathMma2 ? 2 : 0;
+    st->last_path = path;
     em_run_iteration(st, path);
     const IterStatus s = *c->h_status;
     const double cur = s.logL;
@@ -1126,6 +1122,8 @@ int es_ctx_destroy(es_ctx* c) {
         if (!c) return;
         cudaSetDevice(c->device);
         cudaStreamSynchronize(c->stream);
+        for (es_dataset* d : c->live) d->ctx = nullptr;  // live datasets free their own planes later
+        c->live.clear();
         if (c->comm) nccl().CommDestroy(c->comm);
         if (c->h_status) cudaFreeHost(c->h_status);
         if (c->ev0) cudaEventDestroy(c->ev0);
@@ -1183,6 +1181,7 @@ int es_ctx_kernel_time(es_ctx* c, int which, double* ms, int64_t* launches) {
 
 // -------------------------------------------------------------- dataset
 static void finish_dataset(es_ctx* c, es_dataset* ds) {
+    c->live.push_back(ds);
     ds->has_xmap = ds->n_local > 0 && make_event_tmap(&ds->xmap, ds->X, ds->n_local, ds->ld, ds->D);
     double nl = (double)ds->n_local;
     std::vector<double> all = c->allgather_host(&nl, 1);
@@ -1656,6 +1655,7 @@ int es_dataset_info(es_dataset* ds, int64_t* n_local, int64_t* n_global, int64_t
 
 int es_dataset_read_rows(es_dataset* ds, int64_t row0, int64_t n, double* out) {
     return guard([&] {
+        if (!ds->ctx) fail(ES_ERR_RUNTIME, "ContextDestroyed", "the dataset's context was destroyed");
         if (row0 < 0 || n < 0 || row0 + n > ds->n_local) fail(ES_ERR_DATA, "RangeViolation", "rows out of range");
         es_ctx* c = ds->ctx;
         if (n == 0) return;
@@ -1688,6 +1688,15 @@ int es_gmm_em_record_passes(const es_em_state* st, int32_t* passes) {
     return guard([&] {
         if (!st || !passes) fail(ES_ERR_DATA, "InvalidArgument", "null state or output");
         *passes = st->last_npass;
+    });
+}
+
+int es_gmm_em_last_kernel(const es_em_state* st, const char** name) {
+    return guard([&] {
+        if (!st || !name) fail(ES_ERR_DATA, "InvalidArgument", "null state or output");
+        static const char* names[] = {"none (empty shard)", "k_em_diag (FP64)", "strict FP64 (k_em_team / k_em_generic)",
+                                      "k_em_mma<1>", "k_em_mma<2>", "k_em_diag_mixed"};
+        *name = st->last_path < 0 ? "" : names[st->last_path];
     });
 }
 

@@ -439,11 +439,12 @@ __global__ void __launch_bounds__(NTHR, 1) k_score_mma(const __grid_constant__ C
     if (warp == WMMA) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
 }
 
+// ES_SCORE_KERNEL=fp64 scores on the strict FP64 kernel instead.
 bool score_mma_enabled(int D, int K, const ScoreOut& o) {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("ES_SCORE_KERNEL");
-        v = (!e || e[0] == 'm') ? 1 : 0;  // default; "tc" / "simt" select the older kernels
+        v = (e && e[0] == 'f') ? 0 : 1;
     }
     return v == 1 && D <= DM && K <= KMAX && !o.gamma && !o.lnk;
 }

@@ -1,46 +1,12 @@
-// es_tc.cuh — sm_100a building blocks shared by the tensor-core kernels:
-// UMMA shared-memory descriptors (K-major, SWIZZLE_NONE), kind::tf32 MMA issue,
-// TMEM loads, tcgen05 fences, mbarriers, bulk async copies, packed f32x2 math.
+// es_tc.cuh — sm_100a building blocks shared by the tensor-core kernels: TMEM loads,
+// tcgen05 fences, mbarrier waits, TMA / bulk async copies, packed f32x2 math.
 #pragma once
 #include <cstdint>
 
 namespace es {
 namespace tc {
 
-constexpr int kKA = 24;                 // augmented K (16 features + constant + pad)
-constexpr int kTileRows = 128;          // UMMA M
-constexpr int kOpBytes = kTileRows * kKA * 4;  // one 128 x 24 tf32 operand = 12 KB
-constexpr uint32_t kLBO = 128, kSBO = (kKA / 4) * 128;
-// kind::tf32, D=F32, A=B=TF32, K-major, N=128, M=128
-constexpr uint32_t kIdescTF32 = (1u << 4) | (2u << 7) | (2u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
-
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
-    uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
-    d |= (uint64_t)((kLBO >> 4) & 0x3FFF) << 16;
-    d |= (uint64_t)((kSBO >> 4) & 0x3FFF) << 32;
-    d |= (uint64_t)1 << 46;  // descriptor version 1 (sm_100); base offset 0; SWIZZLE_NONE
-    return d;
-}
-
-// byte offset of (row, k) inside one operand buffer
-__device__ __forceinline__ uint32_t op_off(int row, int k) {
-    return (uint32_t)((row >> 3) * kSBO + (k >> 2) * kLBO + (row & 7) * 16 + (k & 3) * 4);
-}
-
-__device__ __forceinline__ uint32_t tf32(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return r;
-}
-
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accum) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(kIdescTF32), "r"(accum));
-}
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     uint32_t r[16];

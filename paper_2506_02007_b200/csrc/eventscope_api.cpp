@@ -91,7 +91,6 @@ es_fit_opts c_opts(const FitOptions& o) {
     r.reg = o.reg ? *o.reg : -1.0;
     r.seed = o.seed;
     r.covariance_type = o.covariance_type == CovarianceType::Diagonal ? ES_COV_DIAG : ES_COV_FULL;
-    if (const char* e = std::getenv("EACGM_SEED")) r.seed = std::strtoull(e, nullptr, 10);
     return r;
 }
 

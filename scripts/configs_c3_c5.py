@@ -20,10 +20,11 @@ def run(tag, n, D, K, cov, iters):
     em.step(iters)
     torch.cuda.synchronize()
     t = (time.perf_counter() - t0) / iters
+    kern = em.last_kernel
     em.close()
     ds.close()
     ctx.close()
-    print(f"{tag}: N={n} D={D} K={K} {cov}: {1 / t:.2f} EM iters/s ({t * 1e3:.1f} ms/iter), "
+    print(f"{tag}: N={n} D={D} K={K} {cov} [{kern}]: {1 / t:.2f} EM iters/s ({t * 1e3:.1f} ms/iter), "
           f"{n * D * 8 / t / 1e9:.0f} GB/s of the FP64 matrix ({n * D * 8 / t / 6547.2e9 * 100:.1f}% of 6.55 TB/s)",
           flush=True)
 

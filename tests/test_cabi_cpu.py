@@ -61,3 +61,26 @@ def test_no_cpu_fallback_without_gpu(lib):
         es.Context(0)
     assert e.value.kind == "Io" and e.value.name == "CudaError"
     assert lib.es_version()
+
+
+def test_eacgm_seed_applies_only_without_explicit_seed(monkeypatch):
+    import paper_2506_02007_b200 as es
+    monkeypatch.setenv("EACGM_SEED", "77")
+    assert es._seed(None) == 77 and es._seed(5) == 5 and es._seed(0) == 0
+    assert es._opts("random", 0.0, 3, None, 5).seed == 5
+    assert es._opts("random", 0.0, 3, None, None).seed == 77
+    monkeypatch.delenv("EACGM_SEED")
+    assert es._seed(None) == 0
+
+
+def test_tensor_inputs_are_dtype_checked():
+    import torch
+
+    import paper_2506_02007_b200 as es
+    with pytest.raises(es.EventscopeError) as e:
+        es._check_tensor(torch.zeros(4, 2, dtype=torch.float32), "float64", 2)
+    assert e.value.name == "InvalidDtype" and e.value.kind == "Data"
+    with pytest.raises(es.EventscopeError) as e:
+        es._check_tensor(torch.zeros(4, dtype=torch.float64), "float64", 2)
+    assert e.value.name == "DimensionMismatch"
+    es._check_tensor(torch.zeros(4, 2, dtype=torch.float64), "float64", 2)

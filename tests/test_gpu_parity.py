@@ -362,3 +362,22 @@ def test_detect_properties_full_size(es):
         if prev is not None:
             assert np.all(f[prev])  # A(delta_i) subset of A(delta_i+1)
         prev = f
+
+
+def test_diag_mixed_pass_parity(es, oracle):
+    """Diagonal covariances, every component >= 2^20 events: the mixed-precision FP32 pass
+    (k_em_diag_mixed) against the oracle (c3's kernel at a parity-testable size)."""
+    n, D, K, iters = 1 << 23, 16, 4, 8
+    ds, X = syn(es, oracle, n, D, K, seed=3)
+    em = es.EM(ds, K, init="random", tol=0.0, max_iter=iters, seed=5, covariance_type="diag")
+    em.step(iters)
+    assert em.last_kernel == "k_em_diag_mixed"
+    m = em.finish()
+    em.close()
+    pi, mu, cov, rep = oracle.fit_em(X, K, init="random", tol=0.0, max_iter=iters, seed=5, covariance_type="diag")
+    assert_params(m, pi, mu, cov)
+    assert np.all(m.covariances[:, ~np.eye(D, dtype=bool)] == 0.0)
+    per_g, per_o = m.fit_report.per_iteration_log_likelihoods, rep["per_iteration_log_likelihoods"]
+    assert np.all(np.abs(per_g - per_o) <= LL_TOL * np.abs(per_o))
+    assert abs(m.fit_report.final_log_likelihood - rep["final_log_likelihood"]) <= LL_TOL * abs(
+        rep["final_log_likelihood"])
