@@ -117,19 +117,22 @@ __global__ void __launch_bounds__(NTD, 1) k_em_diag_mixed(const double* __restri
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const int f = sp + j;
-            pf[j] = (i < n && f < D) ? __ldg(X + (int64_t)f * ld + i) - S.c[f] : 0.0;
+            pf[j] = (i < n && f < D) ? __ldg(X + (int64_t)f * ld + i) : S.c[f];  // centred at stage time
         }
     };
     auto stage = [&](int b) {
         float4* dst = reinterpret_cast<float4*>(&S.x[b][se][sp]);
-        dst[0] = make_float4((float)pf[0], (float)pf[1], (float)pf[2], (float)pf[3]);
-        dst[1] = make_float4((float)pf[4], (float)pf[5], (float)pf[6], (float)pf[7]);
+        const double* cc = S.c + sp;
+        dst[0] = make_float4((float)(pf[0] - cc[0]), (float)(pf[1] - cc[1]), (float)(pf[2] - cc[2]),
+                             (float)(pf[3] - cc[3]));
+        dst[1] = make_float4((float)(pf[4] - cc[4]), (float)(pf[5] - cc[5]), (float)(pf[6] - cc[6]),
+                             (float)(pf[7] - cc[7]));
     };
     uint64_t s1[DG / 2], s2[DG / 2];
-    float nk = 0.f;
+    float nk = 0.f, llf = 0.f;  // llf: sum of ll over the flush window (used from lane k = 0)
+    double llacc = 0.0;
 #pragma unroll
     for (int f = 0; f < DG / 2; ++f) s1[f] = s2[f] = 0;
-    double llacc = 0.0;
     auto flush = [&]() {  // FP32 partial sums -> this lane's FP64 accumulators
         double* a = S.acc[t];
         a[0] += (double)nk;
@@ -145,6 +148,8 @@ __global__ void __launch_bounds__(NTD, 1) k_em_diag_mixed(const double* __restri
             s1[f] = s2[f] = 0;
         }
         nk = 0.f;
+        llacc += (double)llf;
+        llf = 0.f;
     };
     int64_t jt = 0;
     if (blockIdx.x < ntiles) fetch(blockIdx.x);
@@ -180,7 +185,7 @@ __global__ void __launch_bounds__(NTD, 1) k_em_diag_mixed(const double* __restri
 #pragma unroll
             for (int o = 1; o < TSD; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
             const float g = valid ? __fdividef(ex, sum) : 0.f;
-            if (valid && k == 0) llacc += (double)m + (double)__logf(sum);
+            if (valid) llf += m + __logf(sum);  // kept by lane k = 0 of the team
             nk += g;
             const uint64_t g2 = pk2(g, g);
 #pragma unroll

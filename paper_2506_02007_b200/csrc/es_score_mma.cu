@@ -64,6 +64,7 @@ struct SmemS {
     uint16_t plist[NWG][4 * 256];                // extra (event << 4 | component) pairs per warp
     float cst[KMAX], lnf[KMAX], hq[KMAX], tk[KMAX];
     float ec1[KMAX], ec0[KMAX];  // error-bound constants: eps1 ||B_k||_F, eps2 ||b^_k||_2 (U / t_k units)
+    float lpf[KMAX];             // log pi_k (FP32)
     uint64_t xfull[XS], xfree[XS], aeready[NWG], edone[NWG], efree;
     uint32_t tmem;
 };
@@ -104,6 +105,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_score_mma(const __grid_constant__ C
         }
         S.ec1[t] = (float)(0x1p-19 * sqrt(nB));
         S.ec0[t] = (float)(0x1p-22 * sqrt(nb));
+        S.lpf[t] = t < K ? (float)mv.logpi()[t] : 0.f;
     }
     for (int e = t; e < KMAX * DM * DM; e += NTHR) {  // transposed: WT[k][f][r] = W_k[r][f]
         const int k = e / (DM * DM), fr = e % (DM * DM), f = fr / DM, r = fr % DM;
@@ -156,7 +158,6 @@ __global__ void __launch_bounds__(NTHR, 1) k_score_mma(const __grid_constant__ C
         const uint32_t lq = (uint32_t)(32 * q) << 16;
         // per-component constants are read from shared memory (broadcast) where used: kept in
         // registers they would be live across the FP64 refinement (register spills)
-        const float* cst = S.cst;
         const float* lnf = S.lnf;
         const float* hq = S.hq;
         float xnorm = 0.f, xnorm_next = 0.f;  // ||x^||_2 of this thread's event (error bound)
@@ -236,10 +237,13 @@ __global__ void __launch_bounds__(NTHR, 1) k_score_mma(const __grid_constant__ C
             // here: eps1 = 2^-19, eps2 = 2^-22, eps3 = 2^-21.  Cauchy-Schwarz over a gives
             //   ||dU|| <= e = eps1 ||B_k||_F ||x^|| + eps2 ||b^_k|| + eps3 ||U^||,
             //   |q^ - q| <= 2 ||U^|| e + e^2 + 2^-20 q^ (FP32 sum of 16 squares),
-            //   |w^ - w| <= hq (|q^ - q|) + 2^-21 (|w^| + |cst| + 1)   (hq = t_k^2 / 2).
-            float wk[KMAX], dw[KMAX];  // ln_k = wk_k - (cst_k - lnf_k), recomputed where needed
-            float m = -INFINITY, bl = -INFINITY;
-            int km = 0, kb = 0;
+            //   |ln^ - ln| <= hq (|q^ - q|) + 2^-21 (|ln^| + |lognorm| + 1)   (hq = t_k^2 / 2),
+            // and for w = ln + log pi_k (FP32 add) 2^-20 |log pi_k| more.
+            // ln_k (FP32, unweighted) and its bound dw_k; the weighted w_k = ln_k + log pi_k is
+            // formed only when weighted outputs are requested (bound + 2^-20 |log pi_k|)
+            float ln[KMAX], dw[KMAX];
+            float bl = -INFINITY;
+            int kb = 0;
 #pragma unroll
             for (int k0 = 0; k0 < KMAX; k0 += 2) {  // two components per TMEM wait
                 float u[2][16];
@@ -265,19 +269,14 @@ __global__ void __launch_bounds__(NTHR, 1) k_score_mma(const __grid_constant__ C
                     unpack2(qa2, a0, a1);
                     unpack2(qb2, b0, b1);
                     const float q = (a0 + a1) + (b0 + b1);
-                    const float hqq = hq[k] * q;
-                    const float lnk = lnf[k] - hqq;
-                    wk[k] = cst[k] - hqq;
+                    const float lf = lnf[k];
+                    ln[k] = fmaf(-hq[k], q, lf);
                     const float rr = sqrt_approx(q);
                     const float e = fmaf(S.ec1[k], xnorm, fmaf(0x1p-21f, rr, S.ec0[k]));
                     const float dq = fmaf(rr, fmaf(2.f, e, 0x1p-20f * rr), e * e);
-                    dw[k] = fmaf(hq[k], dq, 0x1p-21f * (fabsf(wk[k]) + fabsf(cst[k]) + 1.f));
-                    if (k < K && wk[k] > m) {  // ties -> lowest k
-                        m = wk[k];
-                        km = k;
-                    }
-                    if (k < K && lnk > bl) {
-                        bl = lnk;
+                    dw[k] = fmaf(hq[k], dq, 0x1p-21f * (fabsf(ln[k]) + fabsf(lf) + 1.f));
+                    if (k < K && ln[k] > bl) {  // ties -> lowest k
+                        bl = ln[k];
                         kb = k;
                     }
                 }
@@ -290,27 +289,43 @@ __global__ void __launch_bounds__(NTHR, 1) k_score_mma(const __grid_constant__ C
             // argmax, its contenders and every component with gamma_k dw_k > tau / 8 (the
             // others enter ll = LSE_k w_k with their FP32 value: ll error <= tau + the FP32 LSE
             // rounding).  ovf: every component.
-            const float tau8 = 2.5e-8f * fmaxf(1.f, fabsf(m) - 2.1f);
-            const float dm = dw[km], db = dw[kb];
+            const float db = dw[kb];
             unsigned extra = 0;
 #pragma unroll
-            for (int k = 0; k < KMAX; ++k) {
-                const float lnk = wk[k] - (cst[k] - lnf[k]);
-                bool c = lnk + dw[k] >= bl - db;
-                if (need_w) {
-                    if (refine_all == 1)  // ES_SCORE_REFINE=all: every component with gamma > 1e-6
-                        c = c || wk[k] >= m - 13.9f;
-                    else
-                        c = c || k == km || wk[k] + dw[k] >= m - dm ||
-                            ex2((wk[k] - m) * 1.4426950408889634f) * dw[k] > tau8;
+            for (int k = 0; k < KMAX; ++k)
+                if (ln[k] + dw[k] >= bl - db) extra |= 1u << k;
+            float wk[KMAX];  // weighted FP32 densities (need_w only)
+            float m = -INFINITY;
+            int km = 0;
+            if (need_w) {
+#pragma unroll
+                for (int k = 0; k < KMAX; ++k) {
+                    wk[k] = ln[k] + S.lpf[k];
+                    dw[k] = fmaf(0x1p-20f, fabsf(S.lpf[k]), dw[k]);
+                    if (k < K && wk[k] > m) {
+                        m = wk[k];
+                        km = k;
+                    }
                 }
-                if (refine_all == 3) c = false;  // diagnostics: no FP64 pass at all
-                if (valid && k < K && k != kb && (c || ovf)) extra |= 1u << k;
+                const float tau8 = 2.5e-8f * fmaxf(1.f, fabsf(m) - 2.1f);
+                const float dm = dw[km];
+#pragma unroll
+                for (int k = 0; k < KMAX; ++k) {
+                    bool c;
+                    if (refine_all == 1)  // ES_SCORE_REFINE=all: every component with gamma > 1e-6
+                        c = wk[k] >= m - 13.9f;
+                    else
+                        c = k == km || wk[k] + dw[k] >= m - dm ||
+                            ex2((wk[k] - m) * 1.4426950408889634f) * dw[k] > tau8;
+                    if (c) extra |= 1u << k;
+                }
             }
+            extra = (ovf ? 0xFFu : extra) & ~(1u << kb) & ((1u << K) - 1u);
+            if (!valid || refine_all == 3) extra = 0;  // refine_all 3: diagnostics, no FP64 pass at all
 #ifdef ES_SCORE_COUNT
             if (valid) atomicAdd(&g_score_pairs, (unsigned long long)(1 + __popc(extra)));
 #endif
-            const double lp = (valid && refine_all != 3) ? refine(s, p, kb) : (double)(wk[kb] - (cst[kb] - lnf[kb]));
+            const double lp = (valid && refine_all != 3) ? refine(s, p, kb) : (double)ln[kb];
             // extra pairs: compacted per warp (lane order, then component), one pair per lane
             double* lnv = S.lnv[w];
             const unsigned any = __ballot_sync(0xffffffffu, extra != 0);
@@ -359,7 +374,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_score_mma(const __grid_constant__ C
                     else if ((extra >> k) & 1u)
                         l = lnv[k * TM + p];
                     else
-                        l = (double)(wk[k] - (cst[k] - lnf[k]));
+                        l = (double)ln[k];
                     w64[k] = S.lp64[k] + l;
                     if (k < K && w64[k] > mm) {
                         mm = w64[k];
