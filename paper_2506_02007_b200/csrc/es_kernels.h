@@ -69,6 +69,13 @@ bool em_diag_mixed_supported(int D, int K);
 void launch_em_diag_mixed(const double* X, int64_t n, int64_t ld, int D, int K, const double* model,
                           const double* center, double* partial, int num_sms, int* nblk, cudaStream_t s,
                           LaunchStats& ls);
+// Mixed-precision full-covariance E+M pass (es_em_full.cu) for the shapes the tensor-core pass
+// does not take (D <= 32, K <= 32): FP32 packed arithmetic with per-component centring, FP64
+// statistics; finalize mode 3 (about center + fp32((mu_k - center) xs) / xs).
+bool em_full_mixed_supported(int D, int K);
+void launch_em_full_mixed(const double* X, int64_t n, int64_t ld, int D, int K, const double* model,
+                          const double* center, double xs, double* partial, int num_sms, int* nblk, cudaStream_t s,
+                          LaunchStats& ls);
 // Derive L, W, lognorm, logpi from pi, mu, cov in `model` (all components).
 void launch_derive(double* model, int D, int K, IterStatus* st, cudaStream_t s, LaunchStats& ls);
 // Scoring pass; `blocksum` receives per-CTA [ll_sum, flag_count] pairs.

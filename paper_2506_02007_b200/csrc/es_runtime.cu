@@ -798,7 +798,14 @@ bool em_logl_pass(es_em_state* st, double* out) {
 }
 
 // Iteration paths (the EM pass kernel and its statistics format).
-enum EmIterPath { kPathEmpty = 0, kPathDiag, kPathStrict, kPathMma1, kPathMma2, kPathDiagMixed };
+enum EmIterPath { kPathEmpty = 0, kPathDiag, kPathStrict, kPathMma1, kPathMma2, kPathDiagMixed, kPathFullMixed };
+
+// Full covariances outside the tensor-core pass's shapes: the FP32 k_em_full_mixed pass once
+// every component holds >= kMixedMinNk events (as the tensor-core pass), strict FP64 below.
+bool mixed_full(const es_ctx* c, const es_em_state* st) {
+    return c->precision == 0 && !em_mixed_supported(st->D, st->K) && em_full_mixed_supported(st->D, st->K) &&
+           st->min_nk >= kMixedMinNk && em_mma_enabled();
+}
 
 // The mixed diagonal pass needs >= kOnePassMinNk events in every component (its per-event FP32
 // rounding averages out there), the strict FP64 team kernel otherwise.
@@ -815,6 +822,7 @@ int em_choose_path(const es_em_state* st) {
         const int np = em_mma_passes() ? em_mma_passes() : (st->min_nk >= kOnePassMinNk ? 1 : 2);
         return np == 1 ? kPathMma1 : kPathMma2;
     }
+    if (mixed_full(c, st)) return kPathFullMixed;
     return kPathStrict;
 }
 
@@ -835,6 +843,10 @@ int em_pass_launch(es_em_state* st, int path, int* nblk) {
         case kPathDiag:
             launch_em_diag(ds->X, ds->n_local, ds->ld, D, K, dmodel, part, c->num_sms, nblk, c->stream, c->ls);
             return 2;
+        case kPathFullMixed:
+            launch_em_full_mixed(ds->X, ds->n_local, ds->ld, D, K, dmodel, st->dcenter.as<double>(D), st->xs, part,
+                                 c->num_sms, nblk, c->stream, c->ls);
+            return 3;
         case kPathDiagMixed:
             launch_em_diag_mixed(ds->X, ds->n_local, ds->ld, D, K, dmodel, st->dcenter.as<double>(D), part,
                                  c->num_sms, nblk, c->stream, c->ls);
@@ -851,7 +863,7 @@ int em_pass_launch(es_em_state* st, int path, int* nblk) {
         }
         default:  // an empty shard announces the statistics format the other ranks use
             if (is_diag(st)) return mixed_diag(c, st) ? 4 : 2;
-            if (mixed_em(c, st) && em_mma_enabled()) return 3;
+            if ((mixed_em(c, st) && em_mma_enabled()) || mixed_full(c, st)) return 3;
             return em_path(D, K) != EmPath::Generic ? 1 : 0;
     }
 }
@@ -1695,7 +1707,7 @@ int es_gmm_em_last_kernel(const es_em_state* st, const char** name) {
     return guard([&] {
         if (!st || !name) fail(ES_ERR_DATA, "InvalidArgument", "null state or output");
         static const char* names[] = {"none (empty shard)", "k_em_diag (FP64)", "strict FP64 (k_em_team / k_em_generic)",
-                                      "k_em_mma<1>", "k_em_mma<2>", "k_em_diag_mixed"};
+                                      "k_em_mma<1>", "k_em_mma<2>", "k_em_diag_mixed", "k_em_full_mixed"};
         *name = st->last_path < 0 ? "" : names[st->last_path];
     });
 }

@@ -381,3 +381,21 @@ def test_diag_mixed_pass_parity(es, oracle):
     assert np.all(np.abs(per_g - per_o) <= LL_TOL * np.abs(per_o))
     assert abs(m.fit_report.final_log_likelihood - rep["final_log_likelihood"]) <= LL_TOL * abs(
         rep["final_log_likelihood"])
+
+
+@pytest.mark.parametrize("n,D,K,iters", [(1 << 24, 32, 32, 4), (1 << 22, 24, 12, 6)])
+def test_full_mixed_pass_parity(es, oracle, n, D, K, iters):
+    """Full covariances beyond the tensor-core pass's shapes (the c5 shape D = K = 32 and an
+    odd one), every component >= 2^14 events: the FP32 k_em_full_mixed pass against the oracle."""
+    ds, X = syn(es, oracle, n, D, K, seed=13)
+    em = es.EM(ds, K, init="random", tol=0.0, max_iter=iters, seed=2)
+    em.step(iters)
+    assert em.last_kernel == "k_em_full_mixed"
+    m = em.finish()
+    em.close()
+    pi, mu, cov, rep = oracle.fit_em(X, K, init="random", tol=0.0, max_iter=iters, seed=2)
+    assert_params(m, pi, mu, cov)
+    per_g, per_o = m.fit_report.per_iteration_log_likelihoods, rep["per_iteration_log_likelihoods"]
+    assert np.all(np.abs(per_g - per_o) <= LL_TOL * np.abs(per_o))
+    assert abs(m.fit_report.final_log_likelihood - rep["final_log_likelihood"]) <= LL_TOL * abs(
+        rep["final_log_likelihood"])
