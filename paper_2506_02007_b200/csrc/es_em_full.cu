@@ -4,11 +4,11 @@
 // centring, FP64 statistics; the strict FP64 team / generic kernels remain the path for
 // components with fewer than kMixedMinNk events.
 //
-// One persistent CTA of 256 threads per SM, tiles of T = 32 events, three phases per tile:
-//   E  lane = event, warp w takes components w, w + 8, ...: d = x^ - mu^_k,
-//      z = W'_k d (W' = W / xs, FP32, packed lower-triangular row pairs in shared memory),
+// One persistent CTA of 512 threads per SM, tiles of T = 32 events, three phases per tile:
+//   E  lane = event, warp w takes components w, w + 16: d = x^ - mu^_k,
+//      z = W'_k d (W' = W / xs, FP32, packed lower triangle by feature pair in shared memory),
 //      w_k = log pi_k + lognorm_k - |z|^2 / 2 -> smem
-//   LSE  thread = (event, component group): max / sum over the K components (3 shuffles
+//   LSE  thread = (event, component group): max / sum over the K components (4 shuffles
 //      each), ll, gamma_k -> smem
 //   M  thread = (component, 4 x 4 block of the upper-triangular Gram | 4-vector of s1):
 //      sum over the tile's 32 events of gamma d_a d_b in FP32 registers, then added to the
@@ -28,9 +28,9 @@ namespace {
 constexpr int FD = 32;                      // features (padded)
 constexpr int FK = 32;                      // components (padded)
 constexpr int FT = 32;                      // events per tile
-constexpr int FNT = 256;                    // threads
+constexpr int FNT = 512;                    // threads
 constexpr int FXS = FD + 4;                 // x^ tile row stride (floats): 16-byte rows, conflict-free LDS.128
-constexpr int NPAIR = (FD / 2) * (FD / 2 + 1);  // 272 row pairs per component (rows r: r / 2 + 1 pairs)
+constexpr int NPAIR = (FD / 2) * (FD / 2 + 1);  // 272 (row, feature-pair) entries of the lower triangle
 constexpr int FP = FD * (FD + 1) / 2;       // packed upper triangle
 constexpr int FSK = 1 + FD + FP;            // per-component statistics (padded shape)
 constexpr int NGB = (FD / 4) * (FD / 4 + 1) / 2;  // 36 upper-triangular 4 x 4 Gram blocks
@@ -64,13 +64,13 @@ __device__ __forceinline__ float ex2f(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
-__host__ __device__ constexpr int pair_off(int r) {  // first pair of row r
-    return (r / 2) * (r / 2 + 1) + (r & 1) * (r / 2 + 1);
+__host__ __device__ constexpr int pair_off(int j) {  // feature pair j: rows 2j .. FD-1 from here
+    return j * (FD + 1 - j);
 }
 
 struct FullSmem {
     double acc[FK][FSK];         // FP64 statistics: N_k | s1[32] | s2 packed upper (x^ units)
-    float w2[FK][NPAIR][2];      // W'_k rows as (f, f + 1) pairs, zero padded
+    float w2[FK][NPAIR][2];      // W'_k: for feature pair j, rows 2j .. 31 of (W'_rf, W'_r,f+1)
     float mu[FK][FD];            // mu^_k
     float xt[FT][FXS];           // x^ tile, event-major
     float gw[FK][FT + 1];        // w_k, then gamma_k, per (component, event)
@@ -96,9 +96,9 @@ __global__ void __launch_bounds__(FNT, 1) k_em_full_mixed(const double* __restri
     for (int e = t; e < FK * FSK; e += FNT) (&S.acc[0][0])[e] = 0.0;
     for (int e = t; e < FK * NPAIR; e += FNT) {
         const int k = e / NPAIR, pr = e % NPAIR;
-        int r = 0;
-        while (r + 1 < FD && pair_off(r + 1) <= pr) ++r;
-        const int f = 2 * (pr - pair_off(r));
+        int j = 0;
+        while (j + 1 < FD / 2 && pair_off(j + 1) <= pr) ++j;
+        const int r = 2 * j + (pr - pair_off(j)), f = 2 * j;
         float a = 0.f, b = 0.f;
         if (k < K && r < D) {
             const double* Wr = mv.W() + (int64_t)k * D * D + (int64_t)r * D;
@@ -113,14 +113,14 @@ __global__ void __launch_bounds__(FNT, 1) k_em_full_mixed(const double* __restri
         S.mu[k][f] = (k < K && f < D) ? (float)((mv.mu()[k * D + f] - center[f]) * xs) : 0.f;
     }
     for (int k = t; k < FK; k += FNT) S.cst[k] = k < K ? (float)(mv.logpi()[k] + mv.lognorm()[k]) : -INFINITY;
-    // tile staging: thread t loads events t % 32 of planes 4 (t / 32) .. + 3 (coalesced by plane)
-    const int se = t & (FT - 1), sp = (t >> 5) * 4;
-    double pf[4];
+    // tile staging: thread t loads event t % 32 of planes 2 (t / 32), + 1 (coalesced by plane)
+    const int se = t & (FT - 1), sp = (t >> 5) * 2;
+    double pf[2];
     const int64_t ntiles = (n + FT - 1) / FT;
     auto fetch = [&](int64_t tile) {
         const int64_t i = tile * FT + se;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < 2; ++j) {
             const int f = sp + j;
             pf[j] = (i < n && f < D) ? __ldg(X + (int64_t)f * ld + i) : center[f < D ? f : 0];
         }
@@ -133,37 +133,39 @@ __global__ void __launch_bounds__(FNT, 1) k_em_full_mixed(const double* __restri
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++jt) {
         const int nt = (int)std::min<int64_t>(FT, n - tile * FT);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < 2; ++j) {
             const int f = sp + j;
             S.xt[se][f] = f < D ? (float)((pf[j] - center[f]) * xs) : 0.f;
         }
         __syncthreads();  // tile staged; the previous tile's M phase is done
         if (tile + gridDim.x < ntiles) fetch(tile + gridDim.x);
         // ---------------------------------------------------------------- E phase
+        // lane = event, warp w: components w, w + 16; z_r accumulated over feature pairs j
+        // (rows r >= 2j) as f32x2 partial sums, W' read two rows per 16-byte load
         {
             const int e = lane;
-            uint64_t x2[FD / 2];
-            const float4* xr = reinterpret_cast<const float4*>(&S.xt[e][0]);
-#pragma unroll
-            for (int v = 0; v < FD / 4; ++v) {
-                const float4 q = xr[v];
-                x2[2 * v] = pk2(q.x, q.y);
-                x2[2 * v + 1] = pk2(q.z, q.w);
-            }
             for (int k = warp; k < K; k += FNT / 32) {
-                uint64_t d2[FD / 2];
-                const uint64_t* m2 = reinterpret_cast<const uint64_t*>(&S.mu[k][0]);
+                uint64_t a2[FD];
 #pragma unroll
-                for (int j = 0; j < FD / 2; ++j) d2[j] = sub2(x2[j], m2[j]);
-                const uint64_t* wk = reinterpret_cast<const uint64_t*>(&S.w2[k][0][0]);
+                for (int r = 0; r < FD; ++r) a2[r] = 0;
+                const uint64_t* xr = reinterpret_cast<const uint64_t*>(&S.xt[e][0]);
+                const uint64_t* m2 = reinterpret_cast<const uint64_t*>(&S.mu[k][0]);
+                const ulonglong2* wk = reinterpret_cast<const ulonglong2*>(&S.w2[k][0][0]);
+#pragma unroll
+                for (int j = 0; j < FD / 2; ++j) {
+                    const uint64_t d2 = sub2(xr[j], m2[j]);
+#pragma unroll
+                    for (int r = 2 * j; r < FD; r += 2) {
+                        const ulonglong2 w = wk[(pair_off(j) + r - 2 * j) / 2];
+                        a2[r] = fma2(w.x, d2, a2[r]);
+                        a2[r + 1] = fma2(w.y, d2, a2[r + 1]);
+                    }
+                }
                 float q = 0.f;
 #pragma unroll
                 for (int r = 0; r < FD; ++r) {
-                    uint64_t a2 = 0;
-#pragma unroll
-                    for (int j = 0; j <= r / 2; ++j) a2 = fma2(wk[pair_off(r) + j], d2[j], a2);
                     float za, zb;
-                    up2(a2, za, zb);
+                    up2(a2[r], za, zb);
                     const float z = za + zb;
                     q = fmaf(z, z, q);
                 }
@@ -173,30 +175,30 @@ __global__ void __launch_bounds__(FNT, 1) k_em_full_mixed(const double* __restri
         __syncthreads();
         // --------------------------------------------------------------- LSE phase
         {
-            const int e = t >> 3, g = t & 7;  // event, component group (k = g, g + 8, ...)
-            float wv[FK / 8];
+            const int e = t >> 4, g = t & 15;  // event, component group (k = g, g + 16)
+            float wv[FK / 16];
             float m = -INFINITY;
 #pragma unroll
-            for (int i = 0; i < FK / 8; ++i) {
-                const int k = g + 8 * i;
+            for (int i = 0; i < FK / 16; ++i) {
+                const int k = g + 16 * i;
                 wv[i] = k < K ? S.gw[k][e] : -INFINITY;
                 m = fmaxf(m, wv[i]);
             }
 #pragma unroll
-            for (int o = 1; o < 8; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            for (int o = 1; o < 16; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
             float s = 0.f;
 #pragma unroll
-            for (int i = 0; i < FK / 8; ++i) {
-                wv[i] = g + 8 * i < K ? ex2f((wv[i] - m) * 1.4426950408889634f) : 0.f;
+            for (int i = 0; i < FK / 16; ++i) {
+                wv[i] = g + 16 * i < K ? ex2f((wv[i] - m) * 1.4426950408889634f) : 0.f;
                 s += wv[i];
             }
 #pragma unroll
-            for (int o = 1; o < 8; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            for (int o = 1; o < 16; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
             const bool valid = e < nt;
             const float inv = 1.f / s;
 #pragma unroll
-            for (int i = 0; i < FK / 8; ++i) {
-                const int k = g + 8 * i;
+            for (int i = 0; i < FK / 16; ++i) {
+                const int k = g + 16 * i;
                 if (k < K) S.gw[k][e] = valid ? wv[i] * inv : 0.f;
             }
             if (valid && g == 0) llf += m + __logf(s);
@@ -218,6 +220,7 @@ __global__ void __launch_bounds__(FNT, 1) k_em_full_mixed(const double* __restri
                 const uint64_t ma0 = pk2(ma.x, ma.y), ma1 = pk2(ma.z, ma.w);
                 const uint64_t mb0 = pk2(mb.x, mb.y), mb1 = pk2(mb.z, mb.w);
                 uint64_t acc[4][2] = {};
+#pragma unroll 4
                 for (int e = 0; e < nt; ++e) {
                     const float4 xa = *reinterpret_cast<const float4*>(&S.xt[e][4 * ab]);
                     const float4 xb = *reinterpret_cast<const float4*>(&S.xt[e][4 * bb]);
@@ -256,6 +259,7 @@ __global__ void __launch_bounds__(FNT, 1) k_em_full_mixed(const double* __restri
                 const uint64_t ma0 = pk2(ma.x, ma.y), ma1 = pk2(ma.z, ma.w);
                 uint64_t s0 = 0, s1 = 0;
                 float nk = 0.f;
+#pragma unroll 4
                 for (int e = 0; e < nt; ++e) {
                     const float4 xa = *reinterpret_cast<const float4*>(&S.xt[e][4 * ab]);
                     const float g = gk[e];
@@ -283,7 +287,7 @@ __global__ void __launch_bounds__(FNT, 1) k_em_full_mixed(const double* __restri
     llacc += (double)llf;
     // per-warp ll (threads with g == 0 hold it), fixed order
     {
-        double v = (t & 7) == 0 ? llacc : 0.0;
+        double v = (t & 15) == 0 ? llacc : 0.0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (lane == 0) S.ll[warp] = v;
