@@ -189,12 +189,22 @@ def run_ours(args):
     import paper_2506_02007_b200 as es
 
     rank, world, local = dist_setup(args.gpus)
+    ndev = torch.cuda.device_count()
+    shared = world > ndev  # more ranks than GPUs (a functional check of the multi-rank path only)
+    local = local % ndev
     torch.cuda.set_device(local)
-    if world > 1:
+    exchange = "none"
+    if world > 1 and not shared:
         import torch.distributed as dist
         obj = [es.Context.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         ctx = es.Context(local, rank, world, nccl_id=obj[0])
+        exchange = "nccl (per-iteration stat all-gather over NVLink)"
+    elif world > 1:
+        # NCCL cannot place two ranks on one GPU: exchange through gloo on the host instead
+        from paper_2506_02007_b200.dist import gloo_exchange
+        ctx = es.Context(local, rank, world, exchange=gloo_exchange())
+        exchange = "host gloo (ranks share a GPU: functional check, not a scaling number)"
     else:
         ctx = es.Context(local)
     n_global = args.n or N_GLOBAL
@@ -216,6 +226,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     lib.es_ctx_set_timing(ctx.handle, 1)
     l0 = ctx.launch_count
+    c0 = ctx.collective_count
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         e0.record(stream)
@@ -223,6 +234,7 @@ def run_ours(args):
         e1.record(stream)
         torch.cuda.synchronize()
     em_launches = ctx.launch_count - l0
+    em_collectives = ctx.collective_count - c0
     em_ms = e0.elapsed_time(e1)
     kern_ms, kern_n = ktime(0)
     lib.es_ctx_set_timing(ctx.handle, 0)
@@ -308,20 +320,23 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": em_ms_max / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (SYN-v1 seed 42, device generated)",
         "config": {"workload": WORKLOAD, "N": n_global, "D": D, "K": K, "covariance": "full", "init": "random seed 7",
-                   "l2": "inputs (8.6 GB) larger than L2; no flush", "parallelism": f"rows sharded over {world} GPU(s)"},
+                   "l2": "inputs (8.6 GB) larger than L2; no flush", "parallelism": f"rows sharded over {world} GPU(s)",
+                   "exchange": exchange},
         "roofline": {"bound": "hbm", "kernel": em_kernel, "achieved": ach, "peak": hbm, "unit": "GB/s",
                      "frac": ach / hbm, "peak_source": src, "traffic": args.traffic,
                      "algorithmic_bytes_per_launch": bytes_iter / world, "avg_launch_ms": em_kern_avg,
                      "kernel_share_of_step": kern_ms / em_ms if em_ms else None,
                      "traffic_source": args.traffic_note,
-                     "limiter": "latency of the epilogue warpgroups' per-tile chain (U read, convert, softmax, "
-                                "flush, records ~3.9k clk per warpgroup-tile) and the single TMEM E region; no unit "
-                                "saturated (issue 49%, tensor 47%) - profiles/r01_k_em_mma_pipeline_trace.txt"},
+                     "limiter": "the epilogue warpgroups' per-tile SIMT chain (records, conversion, softmax, "
+                                "Gram flush) at ~49% issue; no unit saturated (tensor 47%, FMA 40%), DRAM bytes = "
+                                "algorithmic - profiles/r02_k_em_mma1_ncu_summary.txt, "
+                                "profiles/r01_k_em_mma_pipeline_trace.txt"},
         "score": {"events_per_s": sc_evs, "ms_per_pass": sc_ms / args.steps, "n_flagged": nflag,
                   "roofline": {"bound": "hbm", "kernel": sc_kernel, "achieved": sc_ach, "peak": hbm,
                                "unit": "GB/s", "frac": sc_ach / hbm,
                                "algorithmic_bytes_per_launch": sc_bytes, "avg_launch_ms": sc_kern_avg}},
         "gpu_launches": em_launches,
+        "nccl_collectives": em_collectives,
         "gpu_launches_score": sc_launches,
         "clocks": clk.summary(),
         "e2e": e2e,
@@ -352,10 +367,10 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override N (debug only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--traffic", type=float, default=8591338000.0 + 4376064.0,
+    ap.add_argument("--traffic", type=float, default=8590144000.0 + 4064256.0,
                     help="dram bytes per EM launch from the committed ncu --set full capture (profiles/)")
     ap.add_argument("--traffic-note", default="dram__bytes_read.sum + dram__bytes_write.sum of k_em_mma<1> at N=2^26, "
-                                              "profiles/r01_k_em_mma1_ncu_summary.txt")
+                                              "profiles/r02_k_em_mma1_ncu_summary.txt")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         spawn_ranks(args.gpus)
