@@ -7,12 +7,13 @@
 // k = component k (2 events per warp, 32 teams).  Event tiles of 256 rows are staged
 // from the planar FP64 matrix with coalesced loads (the next tile held in registers
 // while the current one is evaluated) as FP32 offsets x^ = x - c from the data mean c.
-// Per (event, k), all on the FP32 pipe in packed f32x2 form:
-//   d = x^ - mu^_k (mu^_k = fp32(mu_k - c)),  q = sum_f d_f^2 / sigma2_kf,
-//   w = (log pi_k + lognorm_k) - q / 2;  team max / sum (shuffles) -> ll, gamma_k;
-//   N_k += gamma, s1 += gamma d, s2 += gamma d^2      (FP32 over 32 events per lane,
-// then added to per-lane FP64 accumulators in shared memory), logL in FP64.
-// Statistics are about c + mu^_k (finalize mode 4: diagonal, fp32-rounded centre).
+// Per (event, k), all on the FP32 pipe in packed f32x2 form, in scaled coordinates:
+//   d' = x^ s_k - fp32(mu^_k s_k) (s_k = fp32(1 / sigma_k), mu^_k = fp32(mu_k - c); one FMA),
+//   q = |d'|^2,  w = (log pi_k + lognorm_k) - q / 2;  team max / sum (shuffles) -> ll, gamma_k;
+//   N_k += gamma, s1' += gamma d', s2' += gamma d'^2  (FP32 over 32 events per lane, then
+// added to per-lane FP64 accumulators in shared memory), logL in FP64.  The output unscales
+// (1 / s, 1 / s^2) and re-centres the moments from fp32(mu^ s) / s onto mu^ exactly in FP64:
+// statistics about c + mu^_k (finalize mode 4: diagonal, fp32-rounded centre).
 //
 // Precision: per-event w error ~2^-24 (|x^| + |mu^|) |d| / sigma^2,
 // random across events; the FP32 partial sums cover 32 events before the FP64 flush.
@@ -67,6 +68,15 @@ __device__ __forceinline__ float ex2f(float x) {
     return r;
 }
 
+// 1 / sigma_kf (fp32) and mu^_kf = fp32(mu_kf - c_f): shared by the lanes' set-up and the output
+// re-centring, so both use bit-identical values
+__device__ __forceinline__ float diag_scale(const ModelView& mv, int k, int f) {
+    return (float)sqrt(1.0 / mv.cov()[(int64_t)k * mv.D * mv.D + f * mv.D + f]);
+}
+__device__ __forceinline__ float diag_centre(const ModelView& mv, const double* center, int k, int f) {
+    return (float)(mv.mu()[k * mv.D + f] - center[f]);
+}
+
 struct DiagSmem {
     float x[2][ROWS][DG];        // staged tiles, row-major x^ (FP32)
     double acc[NTD][NACC + 1];   // per-lane FP64 accumulators (+1: bank skew)
@@ -89,21 +99,22 @@ __global__ void __launch_bounds__(NTD, 1) k_em_diag_mixed(const double* __restri
     ModelView mv{K, D, const_cast<double*>(model)};
     for (int f = t; f < DG; f += NTD) S.c[f] = f < D ? center[f] : 0.0;
     for (int e = t; e < NTD * (NACC + 1); e += NTD) (&S.acc[0][0])[e] = 0.0;
-    // this lane's component: mu^ = fp32(mu - c), precisions 1 / sigma^2 (0 on padded features)
-    uint64_t mu2[DG / 2], p2[DG / 2];
+    // this lane's component, in scaled coordinates d' = x^ s - mu^ s (s = 1 / sigma, fp32): one
+    // f32x2 FMA forms d', another accumulates |d'|^2 (0 on padded features)
+    uint64_t s2v[DG / 2], nms2[DG / 2];
     float cst = -INFINITY;
     {
-        float mu[DG], pr[DG];
+        float sc[DG], nms[DG];
 #pragma unroll
         for (int f = 0; f < DG; ++f) {
             const bool on = kact && f < D;
-            mu[f] = on ? (float)(mv.mu()[k * D + f] - center[f]) : 0.f;
-            pr[f] = on ? (float)(1.0 / mv.cov()[(int64_t)k * D * D + f * D + f]) : 0.f;
+            sc[f] = on ? diag_scale(mv, k, f) : 0.f;
+            nms[f] = on ? -(diag_centre(mv, center, k, f) * sc[f]) : 0.f;
         }
 #pragma unroll
         for (int f = 0; f < DG; f += 2) {
-            mu2[f / 2] = pk2(mu[f], mu[f + 1]);
-            p2[f / 2] = pk2(pr[f], pr[f + 1]);
+            s2v[f / 2] = pk2(sc[f], sc[f + 1]);
+            nms2[f / 2] = pk2(nms[f], nms[f + 1]);
         }
         if (kact) cst = (float)(mv.logpi()[k] + mv.lognorm()[k]);
     }
@@ -168,10 +179,10 @@ __global__ void __launch_bounds__(NTD, 1) k_em_diag_mixed(const double* __restri
 #pragma unroll
             for (int v = 0; v < DG / 4; ++v) {
                 const float4 xv = xr[v];
-                d2[2 * v] = sub2(pk2(xv.x, xv.y), mu2[2 * v]);
-                d2[2 * v + 1] = sub2(pk2(xv.z, xv.w), mu2[2 * v + 1]);
-                qa = fma2(mul2(d2[2 * v], p2[2 * v]), d2[2 * v], qa);
-                qb = fma2(mul2(d2[2 * v + 1], p2[2 * v + 1]), d2[2 * v + 1], qb);
+                d2[2 * v] = fma2(pk2(xv.x, xv.y), s2v[2 * v], nms2[2 * v]);
+                d2[2 * v + 1] = fma2(pk2(xv.z, xv.w), s2v[2 * v + 1], nms2[2 * v + 1]);
+                qa = fma2(d2[2 * v], d2[2 * v], qa);
+                qb = fma2(d2[2 * v + 1], d2[2 * v + 1], qb);
             }
             float q0, q1, q2, q3;
             up2(qa, q0, q1);
@@ -220,8 +231,23 @@ __global__ void __launch_bounds__(NTD, 1) k_em_diag_mixed(const double* __restri
             if (p2i == 0) j = 1 + DG + a;  // diagonal entry (a, a)
         }
         double v = 0.0;
-        if (j >= 0)
-            for (int tm = 0; tm < NTEAM; ++tm) v += S.acc[tm * TSD + kc][j];
+        if (j >= 0) {
+            auto tsum = [&](int jj) {
+                double a = 0.0;
+                for (int tm = 0; tm < NTEAM; ++tm) a += S.acc[tm * TSD + kc][jj];
+                return a;
+            };
+            // scaled moments about m = (mu^ s)_fp32 / s -> moments about mu^ (finalize mode 4), FP64
+            v = tsum(j);
+            if (j > 0) {
+                const int f = j <= DG ? j - 1 : j - 1 - DG;
+                const double sf = (double)diag_scale(mv, kc, f);
+                const double mf = (double)diag_centre(mv, center, kc, f);
+                const double dl = (double)(float)(mf * sf) / sf - mf;  // centre of the scaled moments - mu^
+                const double Nk = tsum(0), s1 = tsum(1 + f) / sf;
+                v = j <= DG ? s1 + Nk * dl : v / (sf * sf) + 2.0 * dl * s1 + Nk * dl * dl;
+            }
+        }
         myp[e] = v;
     }
     if (t == 0) {

@@ -91,7 +91,6 @@ __global__ void __launch_bounds__(FNT, 1) k_em_full_mixed(const double* __restri
     FullSmem& S = *reinterpret_cast<FullSmem*>(smraw);
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     ModelView mv{K, D, const_cast<double*>(model)};
-    const float xsf = (float)xs;
     // ---- staging: W' = W / xs as row pairs, mu^ = fp32((mu - c) xs), constants, zeroed stats
     for (int e = t; e < FK * FSK; e += FNT) (&S.acc[0][0])[e] = 0.0;
     for (int e = t; e < FK * NPAIR; e += FNT) {
