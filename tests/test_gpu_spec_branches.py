@@ -181,3 +181,24 @@ def test_acceptance2_parameter_recovery_on_device(es):
     order = np.argsort(m.means[:, 0])
     assert np.all(np.abs(m.means[order, 0] - [-5, 5]) < 0.2)
     assert np.all(np.abs(m.weights[order] - 0.5) < 0.05)
+
+
+def test_dataset_outlives_context(es):
+    """A dataset destroyed after its context frees its own planes (no use-after-free); reading it
+    in between fails with ContextDestroyed."""
+    import ctypes as C
+    lib = es.load_library()
+    h = C.c_void_p()
+    assert lib.es_ctx_create(0, C.byref(h)) == 0
+    d = C.c_void_p()
+    assert lib.es_dataset_generate(h, C.c_uint64(1), C.c_int64(10_000), 4, 2, C.byref(d)) == 0
+    assert lib.es_ctx_destroy(h) == 0
+    out = np.empty((10, 4))
+    assert lib.es_dataset_read_rows(d, C.c_int64(0), C.c_int64(10), C.c_void_p(out.ctypes.data)) != 0
+    assert lib.es_last_error_name().decode() == "ContextDestroyed"
+    assert lib.es_dataset_destroy(d) == 0
+    # the Python layer closes a context's datasets first
+    ctx = es.Context(0)
+    ds = es.Dataset.generate(1, 10_000, 4, 2, ctx=ctx)
+    ctx.close()
+    assert ds.handle is None
