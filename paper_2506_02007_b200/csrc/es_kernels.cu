@@ -1171,55 +1171,80 @@ void launch_em_diag(const double* X, int64_t n, int64_t ld, int D, int K, const 
 // ======================================================= finalize / derive
 // Warp-cooperative Cholesky + inverse of the D x D matrix in A (smem).
 // Writes L, W = L^-1 (smem) and returns logdet in lane 0; false if not PD.
-__device__ bool chol_inv_warp(const double* A, double* L, double* W, int D, double* logdet) {
+// Cholesky A = L L^T and W = L^-1 of a D x D SPD matrix by one warp.  A, L, W in shared
+// memory with row stride ld >= D + 1 (an odd stride in doubles keeps the lanes' rows on
+// distinct banks); column D of L is scratch (1 / L_jj).  Returns false on a numerically
+// singular pivot (the oracle's rule).
+__device__ bool chol_inv_warp(const double* A, double* L, double* W, int D, int ld, double* logdet) {
     const int lane = threadIdx.x & 31;
     bool ok = true;
-    for (int e = lane; e < D * D; e += 32) {
+    for (int e = lane; e < D * ld; e += 32) {
         L[e] = 0.0;
         W[e] = 0.0;
     }
     __syncwarp();
+    // left-looking, lanes over rows i >= j: t_i = A[i][j] - sum_{p<j} L[i][p] L[j][p] (four
+    // independent partial sums); lane j's t_j is the pivot, broadcast by a shuffle
     for (int j = 0; j < D; ++j) {
-        double s = 0.0;
-        for (int p = lane; p < j; p += 32) s = fma(L[j * D + p], L[j * D + p], s);
-        s = warp_sum(s);
-        const double dj = A[j * D + j] - s;
-        // numerical singularity: pivot at or below D 2^-46 of its diagonal entry (as the oracle)
-        if (!(dj > ldexp((double)D, -46) * A[j * D + j]) || !isfinite(dj)) ok = false;
-        const double ljj = sqrt(fmax(dj, 0.0));
-        __syncwarp();
-        if (lane == 0) L[j * D + j] = ljj;
-        __syncwarp();
-        for (int i = j + 1 + lane; i < D; i += 32) {
-            double t = A[i * D + j];
-            for (int p = 0; p < j; ++p) t -= L[i * D + p] * L[j * D + p];
-            L[i * D + j] = t / ljj;
+        double tv[2] = {0.0, 0.0};
+        for (int h = 0; h < 2; ++h) {
+            const int i = j + lane + 32 * h;
+            if (i >= D || (h == 1 && D <= 32)) continue;
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int p = 0;
+            for (; p + 4 <= j; p += 4) {
+                s0 = fma(L[i * ld + p], L[j * ld + p], s0);
+                s1 = fma(L[i * ld + p + 1], L[j * ld + p + 1], s1);
+                s2 = fma(L[i * ld + p + 2], L[j * ld + p + 2], s2);
+                s3 = fma(L[i * ld + p + 3], L[j * ld + p + 3], s3);
+            }
+            for (; p < j; ++p) s0 = fma(L[i * ld + p], L[j * ld + p], s0);
+            tv[h] = A[i * ld + j] - ((s0 + s1) + (s2 + s3));
         }
+        const double dj = __shfl_sync(0xffffffffu, tv[0], 0);  // row i = j sits in lane 0
+        // numerical singularity: pivot at or below D 2^-46 of its diagonal entry (as the oracle)
+        if (!(dj > ldexp((double)D, -46) * A[j * ld + j]) || !isfinite(dj)) ok = false;
+        const double ljj = sqrt(fmax(dj, 0.0));
+        const double rl = 1.0 / ljj;
+        __syncwarp();
+        for (int h = 0; h < 2; ++h) {
+            const int i = j + lane + 32 * h;
+            if (i >= D || (h == 1 && D <= 32)) continue;
+            L[i * ld + j] = i == j ? ljj : tv[h] * rl;
+        }
+        if (lane == 0) L[j * ld + D] = rl;
         __syncwarp();
     }
+    // W = L^-1 by columns (lane c): W[r][c] = (delta_rc - sum_{p=c}^{r-1} L[r][p] W[p][c]) / L[r][r]
     for (int c = lane; c < D; c += 32) {
         for (int r = c; r < D; ++r) {
-            double t = (r == c) ? 1.0 : 0.0;
-            for (int p = c; p < r; ++p) t -= L[r * D + p] * W[p * D + c];
-            W[r * D + c] = t / L[r * D + r];
+            double s0 = (r == c) ? 1.0 : 0.0, s1 = 0.0;
+            int p = c;
+            for (; p + 2 <= r; p += 2) {
+                s0 -= L[r * ld + p] * W[p * ld + c];
+                s1 -= L[r * ld + p + 1] * W[(p + 1) * ld + c];
+            }
+            if (p < r) s0 -= L[r * ld + p] * W[p * ld + c];
+            W[r * ld + c] = (s0 + s1) * L[r * ld + D];
         }
     }
     __syncwarp();
-    double ld = 0.0;
-    if (lane == 0)
-        for (int j = 0; j < D; ++j) ld += log(L[j * D + j]);
-    *logdet = 2.0 * ld;
+    double ldt = 0.0;
+    for (int j = lane; j < D; j += 32) ldt += log(L[j * ld + j]);
+    ldt = warp_sum(ldt);
+    *logdet = 2.0 * ldt;
+    for (int j = lane; j < D; j += 32) L[j * ld + D] = 0.0;
     return ok;
 }
 
 // Per-component derive from pi, mu, cov (block per component, warp 0 works).
 __device__ void derive_component(ModelView mv, int k, double* sA, double* sL, double* sW, IterStatus* st) {
-    const int D = mv.D;
-    for (int e = threadIdx.x; e < D * D; e += blockDim.x) sA[e] = mv.cov()[(int64_t)k * D * D + e];
+    const int D = mv.D, ld = D + 1;
+    for (int e = threadIdx.x; e < D * D; e += blockDim.x) sA[(e / D) * ld + e % D] = mv.cov()[(int64_t)k * D * D + e];
     __syncthreads();
     if (threadIdx.x < 32) {
         double logdet = 0.0;
-        const bool ok = chol_inv_warp(sA, sL, sW, D, &logdet);
+        const bool ok = chol_inv_warp(sA, sL, sW, D, ld, &logdet);
         if (threadIdx.x == 0) {
             if (!ok) atomicAdd(&st->not_pd, 1);
             mv.lognorm()[k] = -0.5 * logdet - 0.5 * D * kLog2Pi;
@@ -1228,15 +1253,16 @@ __device__ void derive_component(ModelView mv, int k, double* sA, double* sL, do
     }
     __syncthreads();
     for (int e = threadIdx.x; e < D * D; e += blockDim.x) {
-        mv.L()[(int64_t)k * D * D + e] = sL[e];
-        mv.W()[(int64_t)k * D * D + e] = sW[e];
+        mv.L()[(int64_t)k * D * D + e] = sL[(e / D) * ld + e % D];
+        mv.W()[(int64_t)k * D * D + e] = sW[(e / D) * ld + e % D];
     }
 }
 
 __global__ void k_derive(double* model, int D, int K, IterStatus* st) {
     extern __shared__ double sm[];
     ModelView mv{K, D, model};
-    derive_component(mv, blockIdx.x, sm, sm + D * D, sm + 2 * D * D, st);
+    const int m = D * (D + 1);
+    derive_component(mv, blockIdx.x, sm, sm + m, sm + 2 * m, st);
 }
 
 void launch_derive(double* model, int D, int K, IterStatus* st, cudaStream_t s, LaunchStats& ls) {
@@ -1245,7 +1271,7 @@ void launch_derive(double* model, int D, int K, IterStatus* st, cudaStream_t s, 
         allow_max_smem(k_derive);
         attr = true;
     }
-    k_derive<<<K, 128, 3 * D * D * sizeof(double), s>>>(model, D, K, st);
+    k_derive<<<K, 128, 3 * D * (D + 1) * sizeof(double), s>>>(model, D, K, st);
     ++ls.launches;
 }
 
@@ -1254,39 +1280,88 @@ void launch_derive(double* model, int D, int K, IterStatus* st, cudaStream_t s, 
 // with T = L_k (whitened statistics) or I (raw), zbar = s1 / N_k.
 // whitened == 3: raw statistics about the centre c + fp32((mu_k - c) xs) / xs
 // (k_em_mma's record centre), given `center` = c and `xs`.
+// `model_in` is the model the EM pass used, `model_out` receives the new one (may alias
+// model_in; distinct buffers let the host keep theta_t while iteration t + 1 is in flight).
+// G > 0: G rank blocks of statistics, summed in rank order (grid K x 1).  G < 0: -G per-CTA
+// partial blocks of one rank (world 1), summed in k_reduce_blocks' fixed order (one warp per
+// entry, lanes over blocks, xor tree) by the gridDim.y CTAs of component k into `red`; the
+// last of them to finish (ticket in tick[k], reset for the next launch) does the M-step.
+constexpr int k_fin_warps = 8 * 2;  // partial-sum entries per finalize CTA (two per warp)
 __global__ void k_finalize(const double* __restrict__ stats, int G, int D, int K, int64_t n_global, double reg,
-                           int whitened, double* model, IterStatus* st, double* record, int t,
-                           const double* __restrict__ center, double xs) {
+                           int whitened, const double* __restrict__ model_in, double* model_out,
+                           IterRecord* st, double* record, int t, const double* __restrict__ center, double xs,
+                           double* red, int* tick) {
     extern __shared__ double sm[];
+    __shared__ int last;
     const int k = blockIdx.x;
-    const int SK = stat_k(D), NE = K * SK, P = packed_size(D);
-    ModelView mv{K, D, model};
+    const int SK = stat_k(D), NE = K * SK, P = packed_size(D), LD = D + 1;
+    ModelView mv{K, D, const_cast<double*>(model_in)};
+    ModelView mo{K, D, model_out};
     double* sS = sm;                 // SK   (summed statistics of component k)
     double* sM = sS + SK;            // D*D
     double* sT = sM + D * D;         // D*D  (T M)
-    double* sA = sT + D * D;         // D*D  (new Sigma)
-    double* sL = sA + D * D;         // D*D
-    double* sW = sL + D * D;         // D*D
-    double* sMu = sW + D * D;        // D
-    for (int e = threadIdx.x; e < SK; e += blockDim.x) {
-        double v = 0.0;
-        for (int g = 0; g < G; ++g) v += stats[(int64_t)g * (NE + 1) + k * SK + e];
-        sS[e] = v;
-    }
-    if (k == 0 && threadIdx.x == 0) {
-        double L = 0.0;
-        for (int g = 0; g < G; ++g) L += stats[(int64_t)g * (NE + 1) + NE];
-        st->logL = L;
-        if (record) record[t] = L;
+    double* sA = sT + D * D;         // D*LD (new Sigma)
+    double* sL = sA + D * LD;        // D*LD
+    double* sW = sL + D * LD;        // D*LD
+    double* sMu = sW + D * LD;       // D
+    if (G > 0) {
+        for (int e = threadIdx.x; e < SK; e += blockDim.x) {
+            double v = 0.0;
+            for (int g = 0; g < G; ++g) v += stats[(int64_t)g * (NE + 1) + k * SK + e];
+            sS[e] = v;
+        }
+        if (k == 0 && threadIdx.x == 0) {
+            double L = 0.0;
+            for (int g = 0; g < G; ++g) L += stats[(int64_t)g * (NE + 1) + NE];
+            st->logL = L;
+            if (record) record[t] = L;
+        }
+    } else {
+        const int nb = -G, lane = threadIdx.x & 31, nw = blockDim.x >> 5, R = gridDim.y;
+        const int cnt = SK + (k == 0 ? 1 : 0);  // component 0 also sums logL (entry NE)
+        for (int i = blockIdx.y * nw + (threadIdx.x >> 5); i < cnt; i += R * nw) {
+            const int64_t col = i < SK ? (int64_t)k * SK + i : NE;
+            double v = 0.0;
+#pragma unroll 4
+            for (int b = lane; b < nb; b += 32) v += stats[(int64_t)b * (NE + 1) + col];
+            v = warp_sum(v);
+            if (lane == 0) red[col] = v;
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int tk = atomicAdd(&tick[k], 1);
+            last = tk == R - 1;
+            if (last) tick[k] = 0;
+        }
+        __syncthreads();
+        if (!last) return;
+        __threadfence();
+        for (int e = threadIdx.x; e < SK; e += blockDim.x) sS[e] = __ldcg(red + (int64_t)k * SK + e);
+        if (k == 0 && threadIdx.x == 0) {
+            const double L = __ldcg(red + NE);
+            st->logL = L;
+            if (record) record[t] = L;
+        }
     }
     __syncthreads();
     const double Nk = sS[0];
-    if (threadIdx.x == 0 && Nk >= 0.0)
-        atomicMax((unsigned long long*)&st->min_nk_inv, ~(unsigned long long)__double_as_longlong(Nk));
+    if (threadIdx.x == 0) st->nk[k] = Nk;
     if (!(Nk >= 1.0)) {  // collapse: N * pi_k < 1; host reseeds
-        if (threadIdx.x == 0) {
-            if (k < 64) atomicOr((unsigned long long*)&st->collapse_lo, 1ull << k);
-            else atomicOr((unsigned long long*)&st->collapse_hi, 1ull << (k - 64));
+        if (threadIdx.x == 0) st->flags[k] = 1;
+        if (model_out != model_in) {  // carry component k over unchanged (the host reseeds it)
+            if (threadIdx.x == 0) {
+                mo.pi()[k] = mv.pi()[k];
+                mo.logpi()[k] = mv.logpi()[k];
+                mo.lognorm()[k] = mv.lognorm()[k];
+            }
+            for (int a = threadIdx.x; a < D; a += blockDim.x) mo.mu()[(int64_t)k * D + a] = mv.mu()[(int64_t)k * D + a];
+            for (int e = threadIdx.x; e < D * D; e += blockDim.x) {
+                const int64_t o = (int64_t)k * D * D + e;
+                mo.cov()[o] = mv.cov()[o];
+                mo.L()[o] = mv.L()[o];
+                mo.W()[o] = mv.W()[o];
+            }
         }
         return;
     }
@@ -1321,16 +1396,16 @@ __global__ void k_finalize(const double* __restrict__ stats, int G, int D, int K
             double v = 0.0;
             for (int p = 0; p <= b; ++p) v = fma(sT[a * D + p], Lold[b * D + p], v);
             if (a == b) v += reg;
-            sA[a * D + b] = v;
-            sA[b * D + a] = v;
+            sA[a * LD + b] = v;
+            sA[b * LD + a] = v;
         }
     } else {
         for (int e = threadIdx.x; e < D * D; e += blockDim.x) {
             const int a = e / D, b = e % D;
             if (a > b) continue;
             const double v = ((whitened == 2 || whitened == 4) && a != b) ? 0.0 : sM[a * D + b] + (a == b ? reg : 0.0);
-            sA[a * D + b] = v;
-            sA[b * D + a] = v;
+            sA[a * LD + b] = v;
+            sA[b * LD + a] = v;
         }
         for (int a = threadIdx.x; a < D; a += blockDim.x) {
             double c0 = cold[a];
@@ -1340,36 +1415,39 @@ __global__ void k_finalize(const double* __restrict__ stats, int G, int D, int K
     }
     __syncthreads();
     // write pi, mu, cov then derive L, W, lognorm, logpi
-    if (threadIdx.x == 0) mv.pi()[k] = Nk / (double)n_global;
-    for (int a = threadIdx.x; a < D; a += blockDim.x) mv.mu()[(int64_t)k * D + a] = sMu[a];
-    for (int e = threadIdx.x; e < D * D; e += blockDim.x) mv.cov()[(int64_t)k * D * D + e] = sA[e];
-    __syncthreads();
+    __syncthreads();  // every read of model_in done (it may alias model_out)
+    if (threadIdx.x == 0) mo.pi()[k] = Nk / (double)n_global;
+    for (int a = threadIdx.x; a < D; a += blockDim.x) mo.mu()[(int64_t)k * D + a] = sMu[a];
+    for (int e = threadIdx.x; e < D * D; e += blockDim.x) mo.cov()[(int64_t)k * D * D + e] = sA[(e / D) * LD + e % D];
     if (threadIdx.x < 32) {
         double logdet = 0.0;
-        const bool ok = chol_inv_warp(sA, sL, sW, D, &logdet);
+        const bool ok = chol_inv_warp(sA, sL, sW, D, LD, &logdet);
         if (threadIdx.x == 0) {
-            if (!ok) atomicAdd(&st->not_pd, 1);
-            mv.lognorm()[k] = -0.5 * logdet - 0.5 * D * kLog2Pi;
-            mv.logpi()[k] = log(Nk / (double)n_global);
+            st->flags[k] = ok ? 0 : 2;
+            mo.lognorm()[k] = -0.5 * logdet - 0.5 * D * kLog2Pi;
+            mo.logpi()[k] = log(Nk / (double)n_global);
         }
     }
     __syncthreads();
     for (int e = threadIdx.x; e < D * D; e += blockDim.x) {
-        mv.L()[(int64_t)k * D * D + e] = sL[e];
-        mv.W()[(int64_t)k * D * D + e] = sW[e];
+        mo.L()[(int64_t)k * D * D + e] = sL[(e / D) * LD + e % D];
+        mo.W()[(int64_t)k * D * D + e] = sW[(e / D) * LD + e % D];
     }
 }
 
 void launch_finalize(const double* stats, int G, int D, int K, int64_t n_global, double reg, int whitened,
-                     double* model, IterStatus* st, double* record, int t, cudaStream_t s, LaunchStats& ls,
-                     const double* center, double xs) {
-    const size_t smem = (size_t)(stat_k(D) + 5 * D * D + D) * sizeof(double);
+                     const double* model_in, double* model_out, IterRecord* st, double* record, int t,
+                     cudaStream_t s, LaunchStats& ls, const double* center, double xs, double* red, int* tick) {
+    const size_t smem = (size_t)(stat_k(D) + 2 * D * D + 3 * D * (D + 1) + D) * sizeof(double);
     static bool attr = false;
     if (!attr) {
         allow_max_smem(k_finalize);
         attr = true;
     }
-    k_finalize<<<K, 128, smem, s>>>(stats, G, D, K, n_global, reg, whitened, model, st, record, t, center, xs);
+    // per-CTA partials (G < 0): R CTAs of 8 warps per component, one entry per warp at a time
+    const int R = G < 0 ? std::max(1, std::min(16, (stat_k(D) + (k_fin_warps - 1)) / k_fin_warps)) : 1;
+    k_finalize<<<dim3(K, R), 256, smem, s>>>(stats, G, D, K, n_global, reg, whitened, model_in, model_out, st, record,
+                                             t, center, xs, red, tick);
     ++ls.launches;
 }
 

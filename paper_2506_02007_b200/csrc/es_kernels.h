@@ -56,9 +56,13 @@ void launch_col_stats(const double* X, int64_t n, int64_t ld, int D, double* scr
 // whitened: 0 raw statistics, 1 whitened (team kernels), 2 raw + diagonal covariance
 // whitened 3: raw statistics about c + fp32((mu_k - c) xs) / xs (k_em_mma), needs center and xs;
 // whitened 4: as 3 with diagonal covariances (k_em_diag_mixed, xs = 1).
+// G < 0: the -G per-CTA partial blocks of a one-rank pass, reduced inside (no k_reduce_blocks).
+// model_in -> model_out (may alias; a collapsed component is carried over unchanged).
+// G < 0 also needs `red` (K * stat_k(D) + 1 doubles) and `tick` (K zeroed ints, left zeroed).
 void launch_finalize(const double* stats, int G, int D, int K, int64_t n_global, double reg, int whitened,
-                     double* model, IterStatus* st, double* record, int t, cudaStream_t s, LaunchStats& ls,
-                     const double* center = nullptr, double xs = 1.0);
+                     const double* model_in, double* model_out, IterRecord* st, double* record, int t,
+                     cudaStream_t s, LaunchStats& ls, const double* center = nullptr, double xs = 1.0,
+                     double* red = nullptr, int* tick = nullptr);
 // Diagonal-covariance E+M pass (FP64 team kernel, D <= 32, K <= 32).
 void launch_em_diag(const double* X, int64_t n, int64_t ld, int D, int K, const double* model, double* partial,
                     int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
@@ -72,6 +76,16 @@ void launch_em_diag_mixed(const double* X, int64_t n, int64_t ld, int D, int K, 
 // Mixed-precision full-covariance E+M pass (es_em_full.cu) for the shapes the tensor-core pass
 // does not take (D <= 32, K <= 32): FP32 packed arithmetic with per-component centring, FP64
 // statistics; finalize mode 3 (about center + fp32((mu_k - center) xs) / xs).
+// Full-covariance E+M pass on tcgen05 for D <= 32, K <= 32 (es_em_wide.cu; BASELINE c5):
+// E-step whitening and M-step Gram on the tensor cores in groups of 4 components; npass = 1
+// one fp16 record per value (>= kOnePassMinNk events per component), 2 fp16 hi + lo records;
+// finalize mode 3.  `workspace`
+// holds em_wide_workspace_bytes() (the per-pass operand images); two launches.
+bool em_wide_supported(int D, int K);
+size_t em_wide_workspace_bytes();
+void launch_em_wide(const double* X, int64_t n, int64_t ld, int D, int K, const double* model, const double* center,
+                    const double* center_host, double xs, bool f32conv, int npass, void* workspace, double* partial,
+                    int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
 bool em_full_mixed_supported(int D, int K);
 void launch_em_full_mixed(const double* X, int64_t n, int64_t ld, int D, int K, const double* model,
                           const double* center, double xs, double* partial, int num_sms, int* nblk, cudaStream_t s,

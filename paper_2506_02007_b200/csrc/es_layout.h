@@ -55,4 +55,13 @@ struct IterStatus {
     uint64_t min_nk_inv;     // ~bits(min_k N_k) (max-reduced; 0 = none): picks the record precision
 };
 
+// Per-iteration record of k_finalize, written straight into mapped pinned host memory
+// (no memset, no copy node): every component's entry is written unconditionally.
+constexpr int kMaxK = 128;
+struct IterRecord {
+    double logL;            // logL of the model the E-step just used
+    double nk[kMaxK];       // N_k of the statistics
+    int32_t flags[kMaxK];   // bit 0: collapse (N_k < 1), bit 1: new covariance not positive definite
+};
+
 }  // namespace es

@@ -342,9 +342,15 @@ struct es_em_state {
     bool converged = false, done = false;
     double prev = 0.0, last = 0.0;
     // the fit's own device buffers (sized once in em_begin, so the pointers a captured
-    // iteration graph holds stay valid for the whole fit) and the graphs per iteration path
-    DevBuf model, backup, partial, stats_local, stats_all, status;
+    // iteration graph holds stay valid for the whole fit) and the graphs per iteration path.
+    // The model has three slots: iteration t reads slot `cur` (theta_t) and writes slot
+    // cur + 1; the next iteration may already be in flight (writing cur + 2) while the host
+    // reads iteration t's status, and theta_t stays intact for a convergence stop.
+    DevBuf model, partial, stats_local, stats_all, status, wide_ws, tick;
     size_t part_cap = 0;
+    int cur = 0;
+    IterRecord* h_rec = nullptr;                    // mapped pinned, one slot per model slot
+    cudaEvent_t done_ev[3] = {}, tev[3][2] = {};   // iteration complete / EM-pass timing per slot
     struct Graph {
         int key;
         cudaGraphExec_t exec;
@@ -353,7 +359,14 @@ struct es_em_state {
     };
     std::vector<Graph> graphs;
     ~es_em_state() {
+        if (ctx) cudaStreamSynchronize(ctx->stream);
         for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+        for (int i = 0; i < 3; ++i) {
+            if (done_ev[i]) cudaEventDestroy(done_ev[i]);
+            for (int j = 0; j < 2; ++j)
+                if (tev[i][j]) cudaEventDestroy(tev[i][j]);
+        }
+        if (h_rec) cudaFreeHost(h_rec);
     }
 };
 
@@ -361,6 +374,13 @@ struct es_em_state {
 namespace {
 
 int64_t mstride(int K, int D) { return ModelView::size(K, D); }
+
+// model slot i (0..2) of a fit; em_model(st) = theta_t
+double* em_model(es_em_state* st, int slot) {
+    const int64_t m = mstride(st->K, st->D);
+    return st->model.as<double>(3 * (size_t)m) + (size_t)slot * m;
+}
+double* em_model(es_em_state* st) { return em_model(st, st->cur); }
 
 void fetch_rows(es_ctx* c, es_dataset* ds, const std::vector<int64_t>& rows, std::vector<double>& out) {
     const int D = ds->D;
@@ -708,7 +728,7 @@ void em_init_model(es_em_state* st, const es_gmm_params* init, const DataStats& 
                         (is_diag(st) && a != b) ? 0.0 : dsx.S[(size_t)a * D + b] + (a == b ? st->reg : 0.0);
         }
     }
-    double* m = st->model.as<double>(mstride(K, D));
+    double* m = em_model(st);
     upload_model(c, m, K, D, pi.data(), mu.data(), cov.data());
     st->min_nk = (double)ds->n_global * *std::min_element(pi.begin(), pi.end());
 }
@@ -750,8 +770,14 @@ void em_begin(es_em_state* st, const es_gmm_params* init) {
         st->partial.as<double>(st->part_cap);
         st->stats_local.as<double>(NE1);
         st->stats_all.as<double>((size_t)NE1 * c->world);
-        st->status.as<IterStatus>(1);
-        st->backup.as<double>(mstride(K, D));
+        CU(cudaMemsetAsync(st->tick.as<int>(K), 0, K * sizeof(int), c->stream));
+        em_model(st, 0);
+        if (!st->h_rec) CU(cudaHostAlloc(&st->h_rec, 3 * sizeof(IterRecord), cudaHostAllocMapped));
+        for (int i = 0; i < 3; ++i) {
+            if (!st->done_ev[i]) CU(cudaEventCreateWithFlags(&st->done_ev[i], cudaEventDisableTiming));
+            for (int j = 0; j < 2; ++j)
+                if (!st->tev[i][j]) CU(cudaEventCreate(&st->tev[i][j]));
+        }
     }
     st->reg = st->opts.reg < 0 ? default_reg(dsx.S, D) : st->opts.reg;
     st->rng = SplitMix64(st->opts.seed);
@@ -774,7 +800,7 @@ bool em_logl_pass(es_em_state* st, double* out) {
     const int K = st->K, D = st->D;
     if (is_diag(st) || !mixed_em(c, st) || !em_mma_enabled() || !ds->has_xmap) return false;
     const int NE1 = stat_total(D, K);
-    double* dmodel = st->model.as<double>(mstride(K, D));
+    double* dmodel = em_model(st);
     double* loc = st->stats_local.as<double>(NE1);
     if (ds->n_local > 0) {
         int nblk = 0;
@@ -798,7 +824,34 @@ bool em_logl_pass(es_em_state* st, double* out) {
 }
 
 // Iteration paths (the EM pass kernel and its statistics format).
-enum EmIterPath { kPathEmpty = 0, kPathDiag, kPathStrict, kPathMma1, kPathMma2, kPathDiagMixed, kPathFullMixed };
+enum EmIterPath {
+    kPathEmpty = 0,
+    kPathDiag,
+    kPathStrict,
+    kPathMma1,
+    kPathMma2,
+    kPathDiagMixed,
+    kPathFullMixed,
+    kPathWide,   // k_em_wide, one fp16 record per value
+    kPathWide2   // k_em_wide, fp16 hi + lo records
+};
+
+// ES_EM_WIDE=0 keeps the FP32 k_em_full_mixed pass where the wide tensor-core pass applies;
+// ES_EM_WIDE=3 (diagnostics) also takes k_em_mma's shapes.  (Read per iteration, so a test
+// can switch it within one process.)
+int em_wide_mode() {
+    const char* e = getenv("ES_EM_WIDE");
+    return (e && e[0] == '0') ? 0 : (e && e[0] == '3') ? 3 : 1;
+}
+
+// Record precision of a k_em_wide iteration: one fp16 record per value once every component
+// held >= kOnePassMinNk events in the previous M-step; hi + lo records otherwise, and in the
+// first iteration (the initial weights are not event counts).  ES_EM_MMA_PASSES forces it.
+int wide_path(const es_em_state* st) {
+    int np = em_mma_passes();
+    if (!np) np = (st->t > 0 && st->min_nk >= kOnePassMinNk) ? 1 : 2;
+    return np == 1 ? kPathWide : kPathWide2;
+}
 
 // Full covariances outside the tensor-core pass's shapes: the FP32 k_em_full_mixed pass once
 // every component holds >= kMixedMinNk events (as the tensor-core pass), strict FP64 below.
@@ -818,11 +871,16 @@ int em_choose_path(const es_em_state* st) {
     const es_dataset* ds = st->ds;
     if (ds->n_local == 0) return kPathEmpty;
     if (is_diag(st)) return mixed_diag(c, st) ? kPathDiagMixed : kPathDiag;
+    if (em_wide_mode() == 3 && c->precision == 0 && em_wide_supported(st->D, st->K) && st->min_nk >= kMixedMinNk)
+        return wide_path(st);
     if (mixed_em(c, st) && em_mma_enabled() && ds->has_xmap) {
         const int np = em_mma_passes() ? em_mma_passes() : (st->min_nk >= kOnePassMinNk ? 1 : 2);
         return np == 1 ? kPathMma1 : kPathMma2;
     }
-    if (mixed_full(c, st)) return kPathFullMixed;
+    if (mixed_full(c, st)) {
+        if (em_wide_mode() && em_wide_supported(st->D, st->K)) return wide_path(st);
+        return kPathFullMixed;
+    }
     return kPathStrict;
 }
 
@@ -832,11 +890,11 @@ int em_choose_path(const es_em_state* st) {
 //   M-step, Cholesky, W = L^-1, collapse flags, logL) -> 40-byte IterStatus to pinned host.
 // The EM pass of an iteration path: launches it and returns the statistics format for
 // k_finalize (*nblk = partial blocks written).
-int em_pass_launch(es_em_state* st, int path, int* nblk) {
+int em_pass_launch(es_em_state* st, int path, int slot, int* nblk) {
     es_ctx* c = st->ctx;
     es_dataset* ds = st->ds;
     const int K = st->K, D = st->D;
-    double* dmodel = st->model.as<double>(mstride(K, D));
+    double* dmodel = em_model(st, slot);
     double* part = st->partial.as<double>(st->part_cap);
     *nblk = 0;
     switch (path) {
@@ -851,6 +909,12 @@ int em_pass_launch(es_em_state* st, int path, int* nblk) {
             launch_em_diag_mixed(ds->X, ds->n_local, ds->ld, D, K, dmodel, st->dcenter.as<double>(D), part,
                                  c->num_sms, nblk, c->stream, c->ls);
             return 4;
+        case kPathWide:
+        case kPathWide2:
+            launch_em_wide(ds->X, ds->n_local, ds->ld, D, K, dmodel, st->dcenter.as<double>(D), st->mean.data(),
+                           st->xs, st->f32conv, path == kPathWide ? 1 : 2, st->wide_ws.get(em_wide_workspace_bytes()),
+                           part, c->num_sms, nblk, c->stream, c->ls);
+            return 3;
         case kPathMma1:
         case kPathMma2:
             launch_em_mma(&ds->xmap, ds->n_local, D, K, dmodel, st->dcenter.as<double>(D), st->mean.data(), st->xs,
@@ -870,31 +934,37 @@ int em_pass_launch(es_em_state* st, int path, int* nblk) {
 
 // Everything of an iteration after the EM pass: fixed-order block reduce -> rank exchange
 // (NCCL all-gather; skipped on one rank) -> k_finalize (rank-ordered sum, M-step, Cholesky,
-// W = L^-1, collapse flags, logL) -> 40-byte IterStatus to pinned host memory.
-void em_tail_launch(es_em_state* st, int path, int nblk, int whitened) {
+// W = L^-1, collapse flags, logL) -> 40-byte IterStatus to pinned host memory.  On one rank
+// without NCCL, k_finalize reduces the per-CTA partials itself (same fixed order).
+// Model slot `slot` -> slot + 1 (mod 3), status slot `slot`.
+void em_tail_launch(es_em_state* st, int path, int slot, int nblk, int whitened) {
     es_ctx* c = st->ctx;
     es_dataset* ds = st->ds;
     const int K = st->K, D = st->D;
     const int NE1 = stat_total(D, K);
-    double* dmodel = st->model.as<double>(mstride(K, D));
     double* part = st->partial.as<double>(st->part_cap);
     double* loc = st->stats_local.as<double>(NE1);
-    if (path != kPathEmpty)
-        launch_reduce_blocks(part, nblk, NE1, loc, c->stream, c->ls);
-    else
-        CU(cudaMemsetAsync(loc, 0, NE1 * 8, c->stream));
     const double* all = loc;
-    if (c->world > 1 || c->mode == 1) {
-        double* ag = st->stats_all.as<double>((size_t)NE1 * c->world);
-        c->allgather(loc, ag, NE1);
-        all = ag;
+    int G = c->world;
+    if (c->world == 1 && c->mode != 1 && path != kPathEmpty) {
+        all = part;
+        G = -nblk;
+    } else {
+        if (path != kPathEmpty)
+            launch_reduce_blocks(part, nblk, NE1, loc, c->stream, c->ls);
+        else
+            CU(cudaMemsetAsync(loc, 0, NE1 * 8, c->stream));
+        if (c->world > 1 || c->mode == 1) {
+            double* ag = st->stats_all.as<double>((size_t)NE1 * c->world);
+            c->allgather(loc, ag, NE1);
+            all = ag;
+        }
     }
-    IterStatus* dst = st->status.as<IterStatus>(1);
-    CU(cudaMemsetAsync(dst, 0, sizeof(IterStatus), c->stream));
-    launch_finalize(all, c->world, D, K, ds->n_global, st->reg, whitened, dmodel, dst, nullptr, st->t, c->stream,
-                    c->ls, st->dcenter.as<double>(D), st->xs);
+    IterRecord* dst = nullptr;  // the slot's record in mapped host memory (device view)
+    CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dst), st->h_rec + slot, 0));
+    launch_finalize(all, G, D, K, ds->n_global, st->reg, whitened, em_model(st, slot), em_model(st, (slot + 1) % 3),
+                    dst, nullptr, st->t, c->stream, c->ls, st->dcenter.as<double>(D), st->xs, loc, st->tick.as<int>(K));
     c->check_launch();
-    CU(cudaMemcpyAsync(c->h_status, dst, sizeof(IterStatus), cudaMemcpyDeviceToHost, c->stream));
 }
 
 // Captures whatever `enqueue` puts on the context stream as a graph (launch and collective
@@ -935,93 +1005,111 @@ bool graphs_enabled(const es_ctx* c) {
     return v == 1 && c->mode != 2;
 }
 
-// One EM iteration (graph replays, or the same sequence launched directly) and the single
-// host synchronisation of the loop: the IterStatus read.  Timing mode records ev0 / ev1 on
-// the stream around the EM pass (a separate graph), so the pass is timed live.
-void em_run_iteration(es_em_state* st, int path) {
+// Enqueues one EM iteration on model slot `slot` (-> slot + 1, status slot `slot`) as graph
+// replays (or the same sequence launched directly), then the slot's completion event; no
+// host synchronisation.  Timing mode brackets the EM pass with the slot's timing events
+// (the pass and the tail are separate graphs then), so the pass is timed live.
+void em_enqueue(es_em_state* st, int path, int slot) {
     es_ctx* c = st->ctx;
     const bool timed = c->timing && path != kPathEmpty;
+    st->last_npass = (path == kPathMma1 || path == kPathWide) ? 1 : (path == kPathMma2 || path == kPathWide2) ? 2 : 0;
+    st->last_path = path;
     if (!graphs_enabled(c)) {
         int nblk = 0;
-        if (timed) c->t_begin();
-        const int wh = em_pass_launch(st, path, &nblk);
-        if (timed) c->t_end(c->em_ms, c->em_launches);
-        em_tail_launch(st, path, nblk, wh);
-        c->sync();
-        return;
-    }
-    auto find = [&](int key) -> es_em_state::Graph* {
-        for (auto& x : st->graphs)
-            if (x.key == key) return &x;
-        return nullptr;
-    };
-    auto replay = [&](es_em_state::Graph* g) {
-        CU(cudaGraphLaunch(g->exec, c->stream));
-        c->ls.launches += g->launches;
-        c->collectives += g->collectives;
-    };
-    if (!timed) {  // key path: one graph for the whole iteration
-        es_em_state::Graph* g = find(4 * path);
+        if (timed) CU(cudaEventRecord(st->tev[slot][0], c->stream));
+        const int wh = em_pass_launch(st, path, slot, &nblk);
+        if (timed) CU(cudaEventRecord(st->tev[slot][1], c->stream));
+        em_tail_launch(st, path, slot, nblk, wh);
+    } else {
+        auto find = [&](int key) -> es_em_state::Graph* {
+            for (auto& x : st->graphs)
+                if (x.key == key) return &x;
+            return nullptr;
+        };
+        auto replay = [&](es_em_state::Graph* g) {
+            CU(cudaGraphLaunch(g->exec, c->stream));
+            c->ls.launches += g->launches;
+            c->collectives += g->collectives;
+        };
+        // one graph per (path, slot, timing): timing mode records the slot's events inside it
+        const int key = 2 * (3 * path + slot) + (timed ? 1 : 0);
+        es_em_state::Graph* g = find(key);
         if (!g) {
-            st->graphs.push_back(capture_graph(c, 4 * path, [&] {
-                int nblk = 0;
-                const int wh = em_pass_launch(st, path, &nblk);
-                em_tail_launch(st, path, nblk, wh);
+            st->graphs.push_back(capture_graph(c, key, [&] {
+                int nblk = 0;  // (external event-record nodes: the events are real, timed records)
+                if (timed) CU(cudaEventRecordWithFlags(st->tev[slot][0], c->stream, cudaEventRecordExternal));
+                const int wh = em_pass_launch(st, path, slot, &nblk);
+                if (timed) CU(cudaEventRecordWithFlags(st->tev[slot][1], c->stream, cudaEventRecordExternal));
+                em_tail_launch(st, path, slot, nblk, wh);
             }));
             g = &st->graphs.back();
         }
         replay(g);
-    } else {  // key 4 path + 1: the pass, 4 path + 2: the tail
-        es_em_state::Graph* gp = find(4 * path + 1);
-        es_em_state::Graph* gt = find(4 * path + 2);
-        if (!gp || !gt) {
-            int nblk = 0, wh = 0;
-            st->graphs.push_back(capture_graph(c, 4 * path + 1, [&] { wh = em_pass_launch(st, path, &nblk); }));
-            st->graphs.push_back(capture_graph(c, 4 * path + 2, [&] { em_tail_launch(st, path, nblk, wh); }));
-            gp = find(4 * path + 1);
-            gt = find(4 * path + 2);
-        }
-        c->t_begin();
-        replay(gp);
-        c->t_end(c->em_ms, c->em_launches);
-        replay(gt);
     }
-    c->sync();
+    CU(cudaEventRecord(st->done_ev[slot], c->stream));
 }
 
-// One EM iteration; returns true when the loop must stop.
-bool em_iterate(es_em_state* st) {
+// Waits for the iteration on `slot` and returns its status (timing mode: adds its EM pass time).
+IterStatus em_wait(es_em_state* st, int slot, int path) {
+    es_ctx* c = st->ctx;
+    CU(cudaEventSynchronize(st->done_ev[slot]));
+    if (c->timing && path != kPathEmpty) {
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, st->tev[slot][0], st->tev[slot][1]));
+        c->em_ms += ms;
+        ++c->em_launches;
+    }
+    // the host view of the slot's IterRecord -> IterStatus (min N_k, collapse mask, not-PD count)
+    const volatile IterRecord* r = st->h_rec + slot;
+    IterStatus s{};
+    s.logL = r->logL;
+    double mn = INFINITY;
+    for (int k = 0; k < st->K; ++k) {
+        const double nk = r->nk[k];
+        const int32_t f = r->flags[k];
+        if (nk >= 0.0) mn = std::min(mn, nk);
+        if (f & 1) {
+            if (k < 64) s.collapse_lo |= 1ull << k;
+            else s.collapse_hi |= 1ull << (k - 64);
+        }
+        if (f & 2) ++s.not_pd;
+    }
+    if (mn < INFINITY) s.min_nk_inv = ~(unsigned long long)__builtin_bit_cast(uint64_t, mn);
+    return s;
+}
+
+// Whether iteration t's status asks for more than recording its logL: a convergence stop,
+// an error, or a collapse reseed (each needs the host to act on the model it produced).
+bool em_needs_host(const es_em_state* st, const IterStatus& s) {
+    if (s.not_pd || s.collapse_lo || s.collapse_hi) return true;
+    return st->opts.tol > 0.0 && st->t >= 1 && std::fabs(s.logL - st->prev) < st->opts.tol * (1.0 + std::fabs(s.logL));
+}
+
+// Host side of iteration t, whose EM pass used model slot `slot` (theta_t) and whose M-step
+// wrote slot + 1: records logL, stops on convergence (theta_t is returned: slot stays
+// current), raises SingularCovariance, reseeds collapsed components in
+// the new model.  Nothing may be in flight on the stream when this acts on the model.
+// Returns true when the loop must stop.
+bool em_after(es_em_state* st, const IterStatus& s, int slot) {
     es_ctx* c = st->ctx;
     es_dataset* ds = st->ds;
     const int K = st->K, D = st->D;
-    double* dmodel = st->model.as<double>(mstride(K, D));
-    double* backup = st->backup.as<double>(mstride(K, D));
-    // theta_t is returned on convergence: keep it (never needed when tol <= 0)
-    const bool can_converge = st->opts.tol > 0.0;
-    if (can_converge)
-        CU(cudaMemcpyAsync(backup, dmodel, mstride(K, D) * 8, cudaMemcpyDeviceToDevice, c->stream));
-    const int path = em_choose_path(st);
-    st->last_npass = path == kPathMma1 ? 1 : path == kPathMma2 ? 2 : 0;
-    st->last_path = path;
-    em_run_iteration(st, path);
-    const IterStatus s = *c->h_status;
     const double cur = s.logL;
     if (s.min_nk_inv) st->min_nk = __builtin_bit_cast(double, ~(unsigned long long)s.min_nk_inv);
     st->per_iter.push_back(cur);
     st->last = cur;
     const int t = st->t++;
-    if (can_converge && t >= 1 && std::fabs(cur - st->prev) < st->opts.tol * (1.0 + std::fabs(cur))) {
-        // converged: theta_t (before this M-step) is returned, final logL = logL_t
-        CU(cudaMemcpyAsync(dmodel, backup, mstride(K, D) * 8, cudaMemcpyDeviceToDevice, c->stream));
-        c->sync();
-        st->converged = true;
+    if (st->opts.tol > 0.0 && t >= 1 && std::fabs(cur - st->prev) < st->opts.tol * (1.0 + std::fabs(cur))) {
+        st->converged = true;  // theta_t (before this M-step) is returned, final logL = logL_t
         return true;
     }
     st->prev = cur;
+    st->cur = (slot + 1) % 3;
     if (s.not_pd) fail(ES_ERR_NUMERIC, "SingularCovariance", "updated covariance is not positive definite");
     if (s.collapse_lo || s.collapse_hi) {
         // reseed mean at a uniform data row, covariance to the
         // data covariance (+reg), weight 1/K then renormalise; at most twice.
+        double* dmodel = em_model(st);
         ModelView mv{K, D, dmodel};
         std::vector<double> pi(K), mu((size_t)K * D), cov((size_t)K * D * D);
         CU(cudaMemcpyAsync(pi.data(), mv.pi(), K * 8, cudaMemcpyDeviceToHost, c->stream));
@@ -1050,6 +1138,54 @@ bool em_iterate(es_em_state* st) {
     }
     st->iterations = t + 1;
     return false;
+}
+
+// ES_EM_SPEC=0 disables enqueueing iteration t + 1 before iteration t's status is read
+// (never in the host-exchange mode, whose all-gather is a synchronous host callback).
+bool spec_enabled(const es_ctx* c) {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ES_EM_SPEC");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1 && c->mode != 2;
+}
+
+// Up to n_iter EM iterations.  Iteration t + 1 is enqueued (on the predicted path: the
+// path only changes with min N_k) before the host waits for iteration t, so the GPU never
+// idles on the host's status read; when iteration t's status needs the host (convergence,
+// an error, a collapse reseed) or changes the path, the speculative iteration is drained and
+// discarded (it wrote only model slot t + 2 and status slot t + 1) and re-enqueued.
+void em_steps(es_em_state* st, int n_iter) {
+    es_ctx* c = st->ctx;
+    int pend = -1;  // path of the iteration already enqueued for t = st->t on slot st->cur
+    for (int i = 0; i < n_iter && !st->done; ++i) {
+        if (st->t >= st->opts.max_iter) {
+            st->done = true;
+            break;
+        }
+        const int slot = st->cur;
+        if (pend < 0) {
+            pend = em_choose_path(st);
+            em_enqueue(st, pend, slot);
+        }
+        const int path = pend;
+        const bool spec = spec_enabled(c) && i + 1 < n_iter && st->t + 1 < st->opts.max_iter;
+        if (spec) em_enqueue(st, path, (slot + 1) % 3);
+        const IterStatus s = em_wait(st, slot, path);
+        bool live = spec;
+        if (live && em_needs_host(st, s)) {
+            CU(cudaStreamSynchronize(c->stream));
+            live = false;
+        }
+        if (em_after(st, s, slot)) st->done = true;
+        if (live && em_choose_path(st) != path) {
+            CU(cudaStreamSynchronize(c->stream));
+            live = false;
+        }
+        pend = live ? path : -1;
+    }
+    if (st->t >= st->opts.max_iter) st->done = true;
 }
 
 }  // namespace
@@ -1707,7 +1843,8 @@ int es_gmm_em_last_kernel(const es_em_state* st, const char** name) {
     return guard([&] {
         if (!st || !name) fail(ES_ERR_DATA, "InvalidArgument", "null state or output");
         static const char* names[] = {"none (empty shard)", "k_em_diag (FP64)", "strict FP64 (k_em_team / k_em_generic)",
-                                      "k_em_mma<1>", "k_em_mma<2>", "k_em_diag_mixed", "k_em_full_mixed"};
+                                      "k_em_mma<1>", "k_em_mma<2>", "k_em_diag_mixed", "k_em_full_mixed",
+                                      "k_em_wide<1>", "k_em_wide<2>"};
         *name = st->last_path < 0 ? "" : names[st->last_path];
     });
 }
@@ -1715,14 +1852,7 @@ int es_gmm_em_last_kernel(const es_em_state* st, const char** name) {
 int es_gmm_em_step(es_em_state* st, int32_t n_iter, int32_t* done) {
     return guard([&] {
         CU(cudaSetDevice(st->ctx->device));
-        for (int i = 0; i < n_iter && !st->done; ++i) {
-            if (st->t >= st->opts.max_iter) {
-                st->done = true;
-                break;
-            }
-            if (em_iterate(st)) st->done = true;
-        }
-        if (st->t >= st->opts.max_iter) st->done = true;
+        em_steps(st, n_iter);
         if (done) *done = st->done ? 1 : 0;
     });
 }
@@ -1732,7 +1862,7 @@ int es_gmm_em_end(es_em_state* st, es_gmm_params* out, es_fit_report* rep, doubl
         es_ctx* c = st->ctx;
         CU(cudaSetDevice(c->device));
         const int K = st->K, D = st->D;
-        double* dmodel = st->model.as<double>(mstride(K, D));
+        double* dmodel = em_model(st);
         double final_ll = st->last;
         if (!st->converged && !em_logl_pass(st, &final_ll))
             final_ll = run_score(c, st->ds, dmodel, K, ScoreOut{}, st->dcenter.as<double>(D), st->mean.data(), st->xs);

@@ -384,15 +384,42 @@ def test_diag_mixed_pass_parity(es, oracle):
 
 
 @pytest.mark.parametrize("n,D,K,iters", [(1 << 24, 32, 32, 4), (1 << 22, 24, 12, 6)])
-def test_full_mixed_pass_parity(es, oracle, n, D, K, iters):
-    """Full covariances beyond the tensor-core pass's shapes (the c5 shape D = K = 32 and an
-    odd one), every component >= 2^14 events: the FP32 k_em_full_mixed pass against the oracle."""
+def test_full_mixed_pass_parity(es, oracle, n, D, K, iters, monkeypatch):
+    """Full covariances beyond k_em_mma's shapes (the c5 shape D = K = 32 and an odd one), every
+    component >= 2^14 events, with the wide tensor-core pass switched off (ES_EM_WIDE=0): the
+    FP32 k_em_full_mixed pass against the oracle."""
+    monkeypatch.setenv("ES_EM_WIDE", "0")
     ds, X = syn(es, oracle, n, D, K, seed=13)
     em = es.EM(ds, K, init="random", tol=0.0, max_iter=iters, seed=2)
     em.step(iters)
     assert em.last_kernel == "k_em_full_mixed"
     m = em.finish()
     em.close()
+    pi, mu, cov, rep = oracle.fit_em(X, K, init="random", tol=0.0, max_iter=iters, seed=2)
+    assert_params(m, pi, mu, cov)
+    per_g, per_o = m.fit_report.per_iteration_log_likelihoods, rep["per_iteration_log_likelihoods"]
+    assert np.all(np.abs(per_g - per_o) <= LL_TOL * np.abs(per_o))
+    assert abs(m.fit_report.final_log_likelihood - rep["final_log_likelihood"]) <= LL_TOL * abs(
+        rep["final_log_likelihood"])
+
+
+@pytest.mark.parametrize("n,D,K,iters", [(1 << 22, 32, 32, 4), (1 << 22, 24, 12, 4), (1 << 23, 32, 4, 4)])
+def test_wide_pass_parity(es, oracle, n, D, K, iters):
+    """The default full-covariance pass beyond k_em_mma's shapes (D, K <= 32; BASELINE c5 is
+    D = K = 32): k_em_wide, E-step whitening and M-step Gram on tcgen05, against the oracle.
+    hi + lo records in the first iteration and while some component holds < 2^20 events; the
+    D = 32, K = 4 case reaches one-fp16 records (2^21 events per component)."""
+    ds, X = syn(es, oracle, n, D, K, seed=13)
+    em = es.EM(ds, K, init="random", tol=0.0, max_iter=iters, seed=2)
+    kern = []
+    for _ in range(iters):
+        em.step(1)
+        kern.append(em.last_kernel)
+    m = em.finish()
+    em.close()
+    assert kern[0] == "k_em_wide<2>", kern
+    if K == 4:
+        assert "k_em_wide<1>" in kern, kern
     pi, mu, cov, rep = oracle.fit_em(X, K, init="random", tol=0.0, max_iter=iters, seed=2)
     assert_params(m, pi, mu, cov)
     per_g, per_o = m.fit_report.per_iteration_log_likelihoods, rep["per_iteration_log_likelihoods"]
