@@ -22,7 +22,7 @@ NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-r
               "-I", INCLUDE] + GENCODE
 CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", "-I", INCLUDE, "-I", "/usr/local/cuda/include"]
 
-CU_SOURCES = ["es_kernels.cu", "es_em_mma.cu", "es_em_diag.cu", "es_em_full.cu", "es_em_wide.cu", "es_score_mma.cu", "es_runtime.cu"]
+CU_SOURCES = ["es_kernels.cu", "es_em_mma.cu", "es_em_diag.cu", "es_em_diag_tc.cu", "es_em_full.cu", "es_em_wide.cu", "es_score_mma.cu", "es_runtime.cu"]
 CXX_SOURCES = ["eventscope_api.cpp"]
 HEADERS = ["es_kernels.h", "es_layout.h", "es_tc.cuh", "es_mma.cuh"]
 

@@ -86,6 +86,14 @@ size_t em_wide_workspace_bytes();
 void launch_em_wide(const double* X, int64_t n, int64_t ld, int D, int K, const double* model, const double* center,
                     const double* center_host, double xs, bool f32conv, int npass, void* workspace, double* partial,
                     int num_sms, int* nblk, cudaStream_t s, LaunchStats& ls);
+// Diagonal E+M pass on tcgen05 (es_em_diag_tc.cu; BASELINE c3): per-event fp16 records of
+// (x^2, x, 1) serve as the E-step A operand (w = A Theta) and the M-step A operand (A^T Gamma);
+// D <= 16, K <= 16, >= kOnePassMinNk events per component; finalize mode 2.  ES_EM_DIAG_TC=0 off.
+bool em_diag_tc_enabled(int D, int K);
+int em_diag_tc_mode();
+void launch_em_diag_tc(const CUtensorMap* xmap, int64_t n, int D, int K, const double* model, const double* center,
+                       const double* center_host, double xs, double* partial, int num_sms, int* nblk, cudaStream_t s,
+                       LaunchStats& ls);
 bool em_full_mixed_supported(int D, int K);
 void launch_em_full_mixed(const double* X, int64_t n, int64_t ld, int D, int K, const double* model,
                           const double* center, double xs, double* partial, int num_sms, int* nblk, cudaStream_t s,

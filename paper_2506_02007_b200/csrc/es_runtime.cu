@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -833,7 +834,8 @@ enum EmIterPath {
     kPathDiagMixed,
     kPathFullMixed,
     kPathWide,   // k_em_wide, one fp16 record per value
-    kPathWide2   // k_em_wide, fp16 hi + lo records
+    kPathWide2,  // k_em_wide, fp16 hi + lo records
+    kPathDiagTc  // k_em_diag_tc (diagonal, tcgen05 E-step quadratic form + M-step moments)
 };
 
 // ES_EM_WIDE=0 keeps the FP32 k_em_full_mixed pass where the wide tensor-core pass applies;
@@ -870,7 +872,12 @@ int em_choose_path(const es_em_state* st) {
     es_ctx* c = st->ctx;
     const es_dataset* ds = st->ds;
     if (ds->n_local == 0) return kPathEmpty;
-    if (is_diag(st)) return mixed_diag(c, st) ? kPathDiagMixed : kPathDiag;
+    if (is_diag(st)) {
+        if (em_diag_tc_mode() == 2 && c->precision == 0 && em_diag_tc_enabled(st->D, st->K) &&
+            st->min_nk >= kMixedMinNk)
+            return kPathDiagTc;
+        return mixed_diag(c, st) ? (em_diag_tc_enabled(st->D, st->K) ? kPathDiagTc : kPathDiagMixed) : kPathDiag;
+    }
     if (em_wide_mode() == 3 && c->precision == 0 && em_wide_supported(st->D, st->K) && st->min_nk >= kMixedMinNk)
         return wide_path(st);
     if (mixed_em(c, st) && em_mma_enabled() && ds->has_xmap) {
@@ -909,6 +916,10 @@ int em_pass_launch(es_em_state* st, int path, int slot, int* nblk) {
             launch_em_diag_mixed(ds->X, ds->n_local, ds->ld, D, K, dmodel, st->dcenter.as<double>(D), part,
                                  c->num_sms, nblk, c->stream, c->ls);
             return 4;
+        case kPathDiagTc:
+            launch_em_diag_tc(&ds->xmap, ds->n_local, D, K, dmodel, st->dcenter.as<double>(D), st->mean.data(), st->xs,
+                              part, c->num_sms, nblk, c->stream, c->ls);
+            return 2;
         case kPathWide:
         case kPathWide2:
             launch_em_wide(ds->X, ds->n_local, ds->ld, D, K, dmodel, st->dcenter.as<double>(D), st->mean.data(),
@@ -926,7 +937,7 @@ int em_pass_launch(es_em_state* st, int path, int slot, int* nblk) {
             return wh ? 1 : 0;
         }
         default:  // an empty shard announces the statistics format the other ranks use
-            if (is_diag(st)) return mixed_diag(c, st) ? 4 : 2;
+            if (is_diag(st)) return (mixed_diag(c, st) && !em_diag_tc_enabled(st->D, st->K)) ? 4 : 2;
             if ((mixed_em(c, st) && em_mma_enabled()) || mixed_full(c, st)) return 3;
             return em_path(D, K) != EmPath::Generic ? 1 : 0;
     }
@@ -1140,6 +1151,16 @@ bool em_after(es_em_state* st, const IterStatus& s, int slot) {
     return false;
 }
 
+// ES_EM_DEBUG=1: one stderr line per EM iteration (path, min N_k, speculation kept)
+bool em_debug() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ES_EM_DEBUG");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 // ES_EM_SPEC=0 disables enqueueing iteration t + 1 before iteration t's status is read
 // (never in the host-exchange mode, whose all-gather is a synchronous host callback).
 bool spec_enabled(const es_ctx* c) {
@@ -1149,6 +1170,23 @@ bool spec_enabled(const es_ctx* c) {
         v = (e && e[0] == '0') ? 0 : 1;
     }
     return v == 1 && c->mode != 2;
+}
+
+// Whether the path of the next iteration is predictable from the current min N_k: the path
+// depends on min N_k only through thresholds (kMixedMinNk, kOnePassMinNk), and min N_k moves
+// by up to ~30% per iteration early in a fit.  Near a threshold (within 2x) the next
+// iteration is not enqueued speculatively: a mispredicted one is a whole discarded EM pass,
+// an unspeculated one costs the status round trip (~40 us).
+bool path_settled(es_em_state* st, int path) {
+    const double m = st->min_nk;
+    ++st->t;  // the next iteration's path (k_em_wide keeps hi + lo records at t = 0)
+    st->min_nk = m * 0.5;
+    const int lo = em_choose_path(st);
+    st->min_nk = m * 2.0;
+    const int hi = em_choose_path(st);
+    st->min_nk = m;
+    --st->t;
+    return lo == path && hi == path;
 }
 
 // Up to n_iter EM iterations.  Iteration t + 1 is enqueued (on the predicted path: the
@@ -1170,7 +1208,7 @@ void em_steps(es_em_state* st, int n_iter) {
             em_enqueue(st, pend, slot);
         }
         const int path = pend;
-        const bool spec = spec_enabled(c) && i + 1 < n_iter && st->t + 1 < st->opts.max_iter;
+        const bool spec = spec_enabled(c) && i + 1 < n_iter && st->t + 1 < st->opts.max_iter && path_settled(st, path);
         if (spec) em_enqueue(st, path, (slot + 1) % 3);
         const IterStatus s = em_wait(st, slot, path);
         bool live = spec;
@@ -1183,6 +1221,9 @@ void em_steps(es_em_state* st, int n_iter) {
             CU(cudaStreamSynchronize(c->stream));
             live = false;
         }
+        if (em_debug())
+            fprintf(stderr, "[es em] t=%d path=%d min_nk=%.0f spec=%d kept=%d\n", st->t - 1, path, st->min_nk,
+                    (int)spec, (int)live);
         pend = live ? path : -1;
     }
     if (st->t >= st->opts.max_iter) st->done = true;
@@ -1844,7 +1885,7 @@ int es_gmm_em_last_kernel(const es_em_state* st, const char** name) {
         if (!st || !name) fail(ES_ERR_DATA, "InvalidArgument", "null state or output");
         static const char* names[] = {"none (empty shard)", "k_em_diag (FP64)", "strict FP64 (k_em_team / k_em_generic)",
                                       "k_em_mma<1>", "k_em_mma<2>", "k_em_diag_mixed", "k_em_full_mixed",
-                                      "k_em_wide<1>", "k_em_wide<2>"};
+                                      "k_em_wide<1>", "k_em_wide<2>", "k_em_diag_tc"};
         *name = st->last_path < 0 ? "" : names[st->last_path];
     });
 }

@@ -364,14 +364,18 @@ def test_detect_properties_full_size(es):
         prev = f
 
 
-def test_diag_mixed_pass_parity(es, oracle):
-    """Diagonal covariances, every component >= 2^20 events: the mixed-precision FP32 pass
-    (k_em_diag_mixed) against the oracle (c3's kernel at a parity-testable size)."""
+@pytest.mark.parametrize("mode,kernel", [("1", "k_em_diag_tc"), ("0", "k_em_diag_mixed")])
+def test_diag_mixed_pass_parity(es, oracle, mode, kernel, monkeypatch):
+    """Diagonal covariances, every component >= 2^20 events: the default tcgen05 pass
+    (k_em_diag_tc, E-step quadratic form and M-step moments on the tensor cores) and the FP32
+    SIMT pass (k_em_diag_mixed, ES_EM_DIAG_TC=0) against the oracle (c3's kernels at a
+    parity-testable size)."""
+    monkeypatch.setenv("ES_EM_DIAG_TC", mode)
     n, D, K, iters = 1 << 23, 16, 4, 8
     ds, X = syn(es, oracle, n, D, K, seed=3)
     em = es.EM(ds, K, init="random", tol=0.0, max_iter=iters, seed=5, covariance_type="diag")
     em.step(iters)
-    assert em.last_kernel == "k_em_diag_mixed"
+    assert em.last_kernel == kernel
     m = em.finish()
     em.close()
     pi, mu, cov, rep = oracle.fit_em(X, K, init="random", tol=0.0, max_iter=iters, seed=5, covariance_type="diag")
@@ -381,6 +385,27 @@ def test_diag_mixed_pass_parity(es, oracle):
     assert np.all(np.abs(per_g - per_o) <= LL_TOL * np.abs(per_o))
     assert abs(m.fit_report.final_log_likelihood - rep["final_log_likelihood"]) <= LL_TOL * abs(
         rep["final_log_likelihood"])
+
+
+def test_diag_tc_c3_shape_parity(es, oracle, monkeypatch):
+    """k_em_diag_tc at c3's K = D = 16 against the oracle.  At a parity-testable N the smallest
+    SYN-v1 component (weight 1/136) holds fewer than the 2^20 events the default path requires,
+    so the pass is forced (ES_EM_DIAG_TC=2): a harder case than the default regime."""
+    monkeypatch.setenv("ES_EM_DIAG_TC", "2")
+    n, D, K, iters = 1 << 24, 16, 16, 6
+    ds, X = syn(es, oracle, n, D, K, seed=3)
+    em = es.EM(ds, K, init="random", tol=0.0, max_iter=iters, seed=5, covariance_type="diag")
+    kern = []
+    for _ in range(iters):
+        em.step(1)
+        kern.append(em.last_kernel)
+    m = em.finish()
+    em.close()
+    assert kern.count("k_em_diag_tc") >= iters - 1, kern
+    pi, mu, cov, rep = oracle.fit_em(X, K, init="random", tol=0.0, max_iter=iters, seed=5, covariance_type="diag")
+    assert_params(m, pi, mu, cov)
+    per_g, per_o = m.fit_report.per_iteration_log_likelihoods, rep["per_iteration_log_likelihoods"]
+    assert np.all(np.abs(per_g - per_o) <= LL_TOL * np.abs(per_o))
 
 
 @pytest.mark.parametrize("n,D,K,iters", [(1 << 24, 32, 32, 4), (1 << 22, 24, 12, 6)])
@@ -403,12 +428,13 @@ def test_full_mixed_pass_parity(es, oracle, n, D, K, iters, monkeypatch):
         rep["final_log_likelihood"])
 
 
-@pytest.mark.parametrize("n,D,K,iters", [(1 << 22, 32, 32, 4), (1 << 22, 24, 12, 4), (1 << 23, 32, 4, 4)])
+@pytest.mark.parametrize("n,D,K,iters", [(1 << 22, 32, 32, 4), (1 << 22, 24, 12, 4), (1 << 24, 32, 4, 4)])
 def test_wide_pass_parity(es, oracle, n, D, K, iters):
     """The default full-covariance pass beyond k_em_mma's shapes (D, K <= 32; BASELINE c5 is
     D = K = 32): k_em_wide, E-step whitening and M-step Gram on tcgen05, against the oracle.
     hi + lo records in the first iteration and while some component holds < 2^20 events; the
-    D = 32, K = 4 case reaches one-fp16 records (2^21 events per component)."""
+    D = 32, K = 4 case reaches one-fp16 records (SYN-v1 weights are (k + 1) / 10, so the
+    smallest component holds ~1.7e6 > 2^20 events at N = 2^24)."""
     ds, X = syn(es, oracle, n, D, K, seed=13)
     em = es.EM(ds, K, init="random", tol=0.0, max_iter=iters, seed=2)
     kern = []
