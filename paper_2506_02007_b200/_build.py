@@ -24,7 +24,7 @@ CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", "-I", INCLUDE, "-
 
 CU_SOURCES = ["es_kernels.cu", "es_em_mma.cu", "es_em_diag.cu", "es_em_diag_tc.cu", "es_em_full.cu", "es_em_wide.cu", "es_score_mma.cu", "es_runtime.cu"]
 CXX_SOURCES = ["eventscope_api.cpp"]
-HEADERS = ["es_kernels.h", "es_layout.h", "es_tc.cuh", "es_mma.cuh"]
+HEADERS = ["es_kernels.h", "es_chol.cuh", "es_layout.h", "es_tc.cuh", "es_mma.cuh"]
 
 
 def _nvcc() -> str:

@@ -18,6 +18,7 @@
 #include <cfloat>
 #include <cmath>
 
+#include "es_chol.cuh"
 #include "es_kernels.h"
 
 namespace es {
@@ -1175,76 +1176,16 @@ void launch_em_diag(const double* X, int64_t n, int64_t ld, int D, int K, const 
 // memory with row stride ld >= D + 1 (an odd stride in doubles keeps the lanes' rows on
 // distinct banks); column D of L is scratch (1 / L_jj).  Returns false on a numerically
 // singular pivot (the oracle's rule).
-__device__ bool chol_inv_warp(const double* A, double* L, double* W, int D, int ld, double* logdet) {
-    const int lane = threadIdx.x & 31;
-    bool ok = true;
-    for (int e = lane; e < D * ld; e += 32) {
-        L[e] = 0.0;
-        W[e] = 0.0;
-    }
-    __syncwarp();
-    // left-looking, lanes over rows i >= j: t_i = A[i][j] - sum_{p<j} L[i][p] L[j][p] (four
-    // independent partial sums); lane j's t_j is the pivot, broadcast by a shuffle
-    for (int j = 0; j < D; ++j) {
-        double tv[2] = {0.0, 0.0};
-        for (int h = 0; h < 2; ++h) {
-            const int i = j + lane + 32 * h;
-            if (i >= D || (h == 1 && D <= 32)) continue;
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-            int p = 0;
-            for (; p + 4 <= j; p += 4) {
-                s0 = fma(L[i * ld + p], L[j * ld + p], s0);
-                s1 = fma(L[i * ld + p + 1], L[j * ld + p + 1], s1);
-                s2 = fma(L[i * ld + p + 2], L[j * ld + p + 2], s2);
-                s3 = fma(L[i * ld + p + 3], L[j * ld + p + 3], s3);
-            }
-            for (; p < j; ++p) s0 = fma(L[i * ld + p], L[j * ld + p], s0);
-            tv[h] = A[i * ld + j] - ((s0 + s1) + (s2 + s3));
-        }
-        const double dj = __shfl_sync(0xffffffffu, tv[0], 0);  // row i = j sits in lane 0
-        // numerical singularity: pivot at or below D 2^-46 of its diagonal entry (as the oracle)
-        if (!(dj > ldexp((double)D, -46) * A[j * ld + j]) || !isfinite(dj)) ok = false;
-        const double ljj = sqrt(fmax(dj, 0.0));
-        const double rl = 1.0 / ljj;
-        __syncwarp();
-        for (int h = 0; h < 2; ++h) {
-            const int i = j + lane + 32 * h;
-            if (i >= D || (h == 1 && D <= 32)) continue;
-            L[i * ld + j] = i == j ? ljj : tv[h] * rl;
-        }
-        if (lane == 0) L[j * ld + D] = rl;
-        __syncwarp();
-    }
-    // W = L^-1 by columns (lane c): W[r][c] = (delta_rc - sum_{p=c}^{r-1} L[r][p] W[p][c]) / L[r][r]
-    for (int c = lane; c < D; c += 32) {
-        for (int r = c; r < D; ++r) {
-            double s0 = (r == c) ? 1.0 : 0.0, s1 = 0.0;
-            int p = c;
-            for (; p + 2 <= r; p += 2) {
-                s0 -= L[r * ld + p] * W[p * ld + c];
-                s1 -= L[r * ld + p + 1] * W[(p + 1) * ld + c];
-            }
-            if (p < r) s0 -= L[r * ld + p] * W[p * ld + c];
-            W[r * ld + c] = (s0 + s1) * L[r * ld + D];
-        }
-    }
-    __syncwarp();
-    double ldt = 0.0;
-    for (int j = lane; j < D; j += 32) ldt += log(L[j * ld + j]);
-    ldt = warp_sum(ldt);
-    *logdet = 2.0 * ldt;
-    for (int j = lane; j < D; j += 32) L[j * ld + D] = 0.0;
-    return ok;
-}
 
 // Per-component derive from pi, mu, cov (block per component, warp 0 works).
 __device__ void derive_component(ModelView mv, int k, double* sA, double* sL, double* sW, IterStatus* st) {
     const int D = mv.D, ld = D + 1;
     for (int e = threadIdx.x; e < D * D; e += blockDim.x) sA[(e / D) * ld + e % D] = mv.cov()[(int64_t)k * D * D + e];
     __syncthreads();
-    if (threadIdx.x < 32) {
+    {
+        __shared__ double csc[2];
         double logdet = 0.0;
-        const bool ok = chol_inv_warp(sA, sL, sW, D, ld, &logdet);
+        const bool ok = chol_inv_any(sA, sL, sW, D, ld, &logdet, csc);
         if (threadIdx.x == 0) {
             if (!ok) atomicAdd(&st->not_pd, 1);
             mv.lognorm()[k] = -0.5 * logdet - 0.5 * D * kLog2Pi;
@@ -1287,6 +1228,22 @@ void launch_derive(double* model, int D, int K, IterStatus* st, cudaStream_t s, 
 // entry, lanes over blocks, xor tree) by the gridDim.y CTAs of component k into `red`; the
 // last of them to finish (ticket in tick[k], reset for the next launch) does the M-step.
 constexpr int k_fin_warps = 8 * 2;  // partial-sum entries per finalize CTA (two per warp)
+#ifdef ES_FIN_TRACE
+// debug timeline (scripts/fin_trace.py): %globaltimer per (CTA, phase), thread 0
+__device__ unsigned long long g_fin_tr[256][8];
+#define FTR(i)                                                                                          \
+    do {                                                                                                \
+        if (threadIdx.x == 0) {                                                                         \
+            unsigned long long v;                                                                       \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));                                        \
+            g_fin_tr[(blockIdx.y * gridDim.x + blockIdx.x) & 255][i] = v;                               \
+        }                                                                                               \
+    } while (0)
+#else
+#define FTR(i) \
+    do {       \
+    } while (0)
+#endif
 __global__ void k_finalize(const double* __restrict__ stats, int G, int D, int K, int64_t n_global, double reg,
                            int whitened, const double* __restrict__ model_in, double* model_out,
                            IterRecord* st, double* record, int t, const double* __restrict__ center, double xs,
@@ -1297,6 +1254,7 @@ __global__ void k_finalize(const double* __restrict__ stats, int G, int D, int K
     const int SK = stat_k(D), NE = K * SK, P = packed_size(D), LD = D + 1;
     ModelView mv{K, D, const_cast<double*>(model_in)};
     ModelView mo{K, D, model_out};
+    FTR(0);
     double* sS = sm;                 // SK   (summed statistics of component k)
     double* sM = sS + SK;            // D*D
     double* sT = sM + D * D;         // D*D  (T M)
@@ -1327,6 +1285,7 @@ __global__ void k_finalize(const double* __restrict__ stats, int G, int D, int K
             v = warp_sum(v);
             if (lane == 0) red[col] = v;
         }
+        FTR(1);
         __threadfence();
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -1336,6 +1295,7 @@ __global__ void k_finalize(const double* __restrict__ stats, int G, int D, int K
         }
         __syncthreads();
         if (!last) return;
+        FTR(2);
         __threadfence();
         for (int e = threadIdx.x; e < SK; e += blockDim.x) sS[e] = __ldcg(red + (int64_t)k * SK + e);
         if (k == 0 && threadIdx.x == 0) {
@@ -1375,6 +1335,7 @@ __global__ void k_finalize(const double* __restrict__ stats, int G, int D, int K
     }
     (void)P;
     __syncthreads();
+    FTR(3);
     const double* Lold = mv.L() + (int64_t)k * D * D;
     const double* cold = mv.mu() + (int64_t)k * D;
     if (whitened == 1) {
@@ -1419,9 +1380,12 @@ __global__ void k_finalize(const double* __restrict__ stats, int G, int D, int K
     if (threadIdx.x == 0) mo.pi()[k] = Nk / (double)n_global;
     for (int a = threadIdx.x; a < D; a += blockDim.x) mo.mu()[(int64_t)k * D + a] = sMu[a];
     for (int e = threadIdx.x; e < D * D; e += blockDim.x) mo.cov()[(int64_t)k * D * D + e] = sA[(e / D) * LD + e % D];
-    if (threadIdx.x < 32) {
+    FTR(4);
+    {
+        __shared__ double csc[2];
         double logdet = 0.0;
-        const bool ok = chol_inv_warp(sA, sL, sW, D, LD, &logdet);
+        const bool ok = chol_inv_any(sA, sL, sW, D, LD, &logdet, csc);
+        FTR(5);
         if (threadIdx.x == 0) {
             st->flags[k] = ok ? 0 : 2;
             mo.lognorm()[k] = -0.5 * logdet - 0.5 * D * kLog2Pi;
@@ -1433,7 +1397,14 @@ __global__ void k_finalize(const double* __restrict__ stats, int G, int D, int K
         mo.L()[(int64_t)k * D * D + e] = sL[(e / D) * LD + e % D];
         mo.W()[(int64_t)k * D * D + e] = sW[(e / D) * LD + e % D];
     }
+    FTR(6);
 }
+
+#ifdef ES_FIN_TRACE
+extern "C" int es_debug_fin_trace(unsigned long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, g_fin_tr, sizeof(g_fin_tr));
+}
+#endif
 
 void launch_finalize(const double* stats, int G, int D, int K, int64_t n_global, double reg, int whitened,
                      const double* model_in, double* model_out, IterRecord* st, double* record, int t,

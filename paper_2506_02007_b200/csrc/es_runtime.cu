@@ -1174,15 +1174,15 @@ bool spec_enabled(const es_ctx* c) {
 
 // Whether the path of the next iteration is predictable from the current min N_k: the path
 // depends on min N_k only through thresholds (kMixedMinNk, kOnePassMinNk), and min N_k moves
-// by up to ~30% per iteration early in a fit.  Near a threshold (within 2x) the next
+// by up to ~35% per iteration early in a fit.  Near a threshold (within 1.5x) the next
 // iteration is not enqueued speculatively: a mispredicted one is a whole discarded EM pass,
 // an unspeculated one costs the status round trip (~40 us).
 bool path_settled(es_em_state* st, int path) {
     const double m = st->min_nk;
     ++st->t;  // the next iteration's path (k_em_wide keeps hi + lo records at t = 0)
-    st->min_nk = m * 0.5;
+    st->min_nk = m / 1.5;
     const int lo = em_choose_path(st);
-    st->min_nk = m * 2.0;
+    st->min_nk = m * 1.5;
     const int hi = em_choose_path(st);
     st->min_nk = m;
     --st->t;
