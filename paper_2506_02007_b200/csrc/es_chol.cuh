@@ -22,14 +22,50 @@ __device__ __forceinline__ double chol_warp_sum(double v) {
 __device__ __noinline__ bool chol_inv_cta(const double* A, double* L, double* W, int D, int ld, double* logdet,
                                           double* scratch) {
     const int t = threadIdx.x, nt = blockDim.x, n2 = D * D;
+    const double thr = ldexp((double)D, -46);
+    bool ok = true;
+    if (n2 <= nt) {  // one element per thread (D <= 16 with 256 threads): indices hoisted
+        const bool on = t < n2;
+        const int i = on ? t / D : 0, c = on ? t - i * D : 0, o = i * ld + c;
+        if (on) {
+            L[o] = c <= i ? A[o] : 0.0;
+            W[o] = c == i ? 1.0 : 0.0;
+        }
+        __syncthreads();
+        for (int j = 0; j < D; ++j) {
+            const double piv = L[j * ld + j];
+            if (!(piv > thr * A[j * ld + j]) || !isfinite(piv)) ok = false;
+            const double rl = rsqrt(fmax(piv, 0.0));
+            if (on) {
+                if (c == j && i > j) L[o] *= rl;
+                if (i == j && c <= j) W[o] *= rl;
+                if (i == j && c == j) L[o] = piv * rl;
+            }
+            __syncthreads();
+            if (on && i > j) {
+                const double lij = L[i * ld + j];
+                if (c > j && c <= i) L[o] = fma(-lij, L[c * ld + j], L[o]);
+                if (c <= j) W[o] = fma(-lij, W[j * ld + c], W[o]);
+            }
+            __syncthreads();
+        }
+        if (t < 32) {
+            double v = 0.0;
+            for (int r = t; r < D; r += 32) v += log(L[r * ld + r]);
+            v = chol_warp_sum(v);
+            if (t == 0) scratch[0] = v;
+        }
+        __syncthreads();
+        *logdet = 2.0 * scratch[0];
+        __syncthreads();
+        return ok;
+    }
     for (int e = t; e < n2; e += nt) {
         const int i = e / D, c = e % D;
         L[i * ld + c] = c <= i ? A[i * ld + c] : 0.0;
         W[i * ld + c] = c == i ? 1.0 : 0.0;
     }
     __syncthreads();
-    const double thr = ldexp((double)D, -46);
-    bool ok = true;
     for (int j = 0; j < D; ++j) {
         const double piv = L[j * ld + j];
         // numerical singularity: pivot at or below D 2^-46 of its diagonal entry (as the oracle)
