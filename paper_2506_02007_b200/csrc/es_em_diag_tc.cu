@@ -19,7 +19,8 @@
 // Record (per event, 6 chunks of 16 fp16 statistics; group g holds features 7g .. 7g + 6):
 //   chunk 2g     (hi): hi(x^_f^2) | hi(x^_f) | 1 | 0        slots 0-6 | 7-13 | 14 | 15
 //   chunk 2g + 1 (lo): lo(x^_f^2) | lo(x^_f) | 0 | 0
-// E-step per group: hi x Theta_hi, hi x Theta_lo, lo x Theta_hi (3 dispatches, M128 N16 K16),
+// E-step per group: hi x [Theta_hi | Theta_lo] (M128 N32 K16) and lo x Theta_hi (M128 N16 K16):
+// 6 dispatches (each tcgen05.mma costs ~60-90 cycles of the in-order tensor pipe however small),
 // Theta = coefficients / t_k (t_k a power of two: largest |entry| in (2^12, 2^13]), the group's
 // constant -1/2 sum_{f in g} p mu^2 (+ log pi + lognorm for g = 0) in its '1' slot, so every
 // running sum of the FP32 accumulator (truncated ~1 ulp per dispatch, scripts/umma_probe.cu) is
@@ -45,10 +46,7 @@
 #define ES_DTC_NACC 1
 #endif
 #ifndef ES_DTC_NWG  // epilogue warpgroups
-#define ES_DTC_NWG 2
-#endif
-#ifndef ES_DTC_EACC  // E-step accumulators per warpgroup: 1, or one per record group (3)
-#define ES_DTC_EACC 1
+#define ES_DTC_NWG 3
 #endif
 #ifndef ES_DTC_CST  // 1: log pi_k + lognorm_k added in FP32 after the E-step instead of in Theta
 #define ES_DTC_CST 1
@@ -72,24 +70,26 @@ constexpr uint32_t GRB = 2 * (KC / 8) * SGB;     // gamma record (hi | lo): 8 KB
 constexpr float GSCALE = 1024.f;                 // gamma records hold 2^10 gamma (normal fp16 range)
 constexpr int NWG_DTC = ES_DTC_NWG;
 constexpr int nthr_dtc() { return 128 * NWG_DTC + 96; }
-constexpr int XSD = NWG_DTC >= 3 ? 2 : 4;        // FP64 tile stages
+// FP64 tile stages: a multiple of NWG, so that a stage's previous tile was converted by the same
+// warpgroup (a converter two mbarrier phases ahead of its stage would pass the parity wait)
+constexpr int XSD = NWG_DTC >= 3 ? NWG_DTC : 4;
 
 struct SmemDT {
     double xd[XSD][DG * TM];                     // 64 KB  FP64 tiles (planar, TMA destination)
     unsigned char rec[NWG_DTC][2][RECB];         // 96 KB  statistic records (double-buffered per WG)
-    unsigned char slack[4 * SGB];                // the M-step (M = 128) reads 4 slot groups past a record
-    unsigned char grec[NWG_DTC][GRB];            // gamma records
-    unsigned char bth[NG][512], btl[NG][512];    // Theta hi / lo, K-major 16 components x 16 slots
+    unsigned char grec[NWG_DTC][GRB];            // gamma records; also the 4 slot groups the M-step
+                                                 // (M = 128) reads past the last record (junk rows)
+    unsigned char bt[NG][1024];                  // [Theta_hi | Theta_lo]: K-major 32 rows (hi: components, lo) x 16 slots
     float tk[KC], cst[KC];
     double wred[4 * NWG_DTC];
     uint64_t xfull[XSD], xfree[XSD], aeready[NWG_DTC], edone[NWG_DTC], mready[NWG_DTC], mdone[NWG_DTC];
     uint32_t tmem;
 };
 
-constexpr int EACC = ES_DTC_EACC;
-constexpr int ECOL = 0;                          // E accumulators of WG w: columns 16 EACC w
-constexpr int MCOL = (16 * EACC * NWG_DTC + 31) / 32 * 32;  // M accumulators of WG w: MCOL + 32 NACC w
-static_assert(MCOL + 32 * NACC * NWG_DTC <= 256 && 16 * EACC * NWG_DTC <= MCOL, "TMEM columns");
+constexpr int ECOL = 0;                          // E accumulator of WG w: columns 32 w (hi Theta_hi + lo Theta_hi | hi Theta_lo)
+constexpr int MCOL = 32 * NWG_DTC;               // M accumulators of WG w: MCOL + 32 NACC w
+static_assert(sizeof(((SmemDT*)0)->grec) >= 4 * SGB, "junk rows of the last record");
+static_assert(MCOL + 32 * NACC * NWG_DTC <= 256, "TMEM columns");
 
 }  // namespace
 
@@ -108,7 +108,6 @@ __global__ void __launch_bounds__(nthr_dtc(), 1)
 
     // ------------------------------------------------------------------ staging
     for (int e = t; e < XSD * DG * TM; e += NTHR) (&S.xd[0][0])[e] = 0.0;  // planes >= D stay zero
-    for (int e = t; e < (int)sizeof(S.slack) / 4; e += NTHR) reinterpret_cast<uint32_t*>(S.slack)[e] = 0u;
     if (t < KC) {  // t_k: power of two putting component k's largest |coefficient| into (2^12, 2^13]
         const int k = t;
         float tk = 1.f;
@@ -159,8 +158,8 @@ __global__ void __launch_bounds__(nthr_dtc(), 1)
         }
         const __half hh = __double2half(th);
         const __half hl = __double2half(th - (double)__half2float(hh));
-        *reinterpret_cast<__half*>(S.bth[g] + kmaj(k, s)) = hh;
-        *reinterpret_cast<__half*>(S.btl[g] + kmaj(k, s)) = hl;
+        *reinterpret_cast<__half*>(S.bt[g] + kmaj(k, s)) = hh;
+        *reinterpret_cast<__half*>(S.bt[g] + kmaj(KC + k, s)) = hl;
     }
     if (warp == WE) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(&S.tmem)));
@@ -272,18 +271,12 @@ __global__ void __launch_bounds__(nthr_dtc(), 1)
             const bool valid = tile_of(j) * TM + p < n;
             mbar_wait(su32(&S.edone[w]), (uint32_t)(jj & 1));
             tc_fence_after();
-            float a[16];
-            tmem_ld16(tmem + lq + ECOL + 16 * EACC * w, a);
-            if (EACC == 3) {
-                float a1[16], a2[16];
-                tmem_ld16(tmem + lq + ECOL + 16 * EACC * w + 16, a1);
-                tmem_ld16(tmem + lq + ECOL + 16 * EACC * w + 32, a2);
-                tmem_wait_ld();
+            float a[16], b[16];
+            tmem_ld16(tmem + lq + ECOL + 32 * w, a);
+            tmem_ld16(tmem + lq + ECOL + 32 * w + 16, b);
+            tmem_wait_ld();
 #pragma unroll
-                for (int k = 0; k < 16; ++k) a[k] = (a[k] + a1[k]) + a2[k];
-            } else {
-                tmem_wait_ld();
-            }
+            for (int k = 0; k < 16; ++k) a[k] += b[k];
             float wk[KC];
             float mx = -INFINITY;
 #pragma unroll
@@ -323,10 +316,12 @@ __global__ void __launch_bounds__(nthr_dtc(), 1)
         }
         if (Jw > 0) flush(Jw - 1);
         // -------------------------------------------------------------- output
-        // rows (group q, slot lane) of every WG -> FP64 scratch (the FP64 tile ring is idle now)
+        // rows (group q, slot lane) of every WG -> FP64 scratch
         named_sync(1, 128 * NWG);
-        double* sc = &S.xd[0][0];  // [NWG][NG][32 slots: hi chunk | lo chunk][KC]
-        static_assert(NWG_DTC * NG * 32 * KC <= XSD * DG * TM, "output scratch");
+        // [NWG][NG][32 slots: hi chunk | lo chunk][KC] in the record buffers: every MMA that read
+        // them completed (each WG waited for its last M-step before the barrier above)
+        double* sc = reinterpret_cast<double*>(&S.rec[0][0][0]);
+        static_assert(NWG_DTC * NG * 32 * KC * sizeof(double) <= sizeof(S.rec), "output scratch");
         if (q < NG) {
 #pragma unroll
             for (int k = 0; k < KC; ++k)
@@ -398,29 +393,26 @@ __global__ void __launch_bounds__(nthr_dtc(), 1)
     } else if (warp == WE) {
         // ==================================================== E-step MMA issuer
         if (lane == 0) {
-            constexpr uint32_t idesc = idesc_f16(128, 16, 0);
-            uint64_t bh[NG], bl[NG];
+            constexpr uint32_t idesc32 = idesc_f16(128, 32, 0), idesc16 = idesc_f16(128, 16, 0);
+            uint64_t bhl[NG];
 #pragma unroll
-            for (int g = 0; g < NG; ++g) {
-                bh[g] = sdesc(su32(S.bth[g]), 128, 256);
-                bl[g] = sdesc(su32(S.btl[g]), 128, 256);
-            }
+            for (int g = 0; g < NG; ++g) bhl[g] = sdesc(su32(S.bt[g]), 128, 256);  // rows 0-15: Theta_hi
             for (int64_t je = 0; je < J; ++je) {
                 const int w = (int)(je % NWG);
                 const int64_t jl = je / NWG;
                 mbar_wait_sleep(su32(&S.aeready[w]), (uint32_t)(jl & 1));
                 tc_fence_after();
                 const uint32_t rb = su32(S.rec[w][jl & 1]);
+                const uint32_t d = tmem + ECOL + 32 * w;
 #pragma unroll
                 for (int g = 0; g < NG; ++g) {
-                    const uint32_t d = tmem + ECOL + 16 * EACC * w + (EACC == 3 ? 16 * g : 0);
                     // K-major A: chunk (slot groups 2 ch, 2 ch + 1; LBO = slot-group stride),
-                    // rows = events (SBO = 128 B per 8 events)
+                    // rows = events (SBO = 128 B per 8 events).  hi chunk x [Theta_hi | Theta_lo]
+                    // (N = 32: columns 0-15 and 16-31), lo chunk x Theta_hi onto columns 0-15.
                     const uint64_t ah = sdesc(rb + (4 * g) * SGB, SGB, 128);
                     const uint64_t alo = sdesc(rb + (4 * g + 2) * SGB, SGB, 128);
-                    mma_f16(d, ah, bh[g], idesc, (EACC == 1 && g > 0) ? 1u : 0u);
-                    mma_f16(d, ah, bl[g], idesc, 1u);
-                    mma_f16(d, alo, bh[g], idesc, 1u);
+                    mma_f16(d, ah, bhl[g], idesc32, g > 0 ? 1u : 0u);
+                    mma_f16(d, alo, bhl[g], idesc16, 1u);
                 }
                 commit(&S.edone[w]);
             }

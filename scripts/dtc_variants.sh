@@ -10,8 +10,9 @@ for spec in "$@"; do
   mkdir -p $L/v_$name
   nvcc $flags -O3 -std=c++17 -lineinfo -Xcompiler -fPIC --expt-relaxed-constexpr -I include \
     -gencode arch=compute_100a,code=sm_100a -c paper_2506_02007_b200/csrc/$src -o $L/v_$name/$src.o &
+  pids="$pids $!"
 done
-wait
+for p in $pids; do wait $p; done  # set -e: a failed compile stops here
 for spec in "$@"; do
   name=${spec%%:*}
   objs=$(ls $L/obj/*.o | grep -v "/$src.o")
