@@ -1453,40 +1453,94 @@ void launch_hist8(const double* keys, int64_t n, int shift, uint64_t prefix_mask
 
 // ============================================================== compaction
 constexpr int kChunkC = 4096;
+static_assert(kChunkC == 16 * kBlock, "compaction: 16 flags per thread");
+
+// Flags are 0 / 1 bytes; a thread takes 16 consecutive ones (one 16-byte load when the chunk is
+// whole and the buffer 16-byte aligned) and counts them with popc; the per-chunk and per-block
+// scans are warp-shuffle scans (integer, so any order is exact).
+__device__ __forceinline__ int flags16(const uint8_t* __restrict__ flags, int64_t i0, int64_t n, bool vec,
+                                       uint32_t (&w)[4]) {
+    if (vec && i0 + 16 <= n) {
+        const uint4 v = *reinterpret_cast<const uint4*>(flags + i0);
+        w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
+    } else {
+        for (int q = 0; q < 4; ++q) {
+            uint32_t x = 0;
+            for (int b = 0; b < 4; ++b) {
+                const int64_t i = i0 + 4 * q + b;
+                if (i < n && flags[i]) x |= 1u << (8 * b);
+            }
+            w[q] = x;
+        }
+    }
+    return __popc(w[0] & 0x01010101u) + __popc(w[1] & 0x01010101u) + __popc(w[2] & 0x01010101u) +
+           __popc(w[3] & 0x01010101u);
+}
+
+// exclusive block scan of one int per thread (blockDim.x = kBlock); returns the block total in *tot
+__device__ __forceinline__ int block_excl_scan(int v, int* wsum, int* tot) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int s = lane < nw ? wsum[lane] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, s, d);
+            if (lane >= d) s += y;
+        }
+        if (lane < nw) wsum[lane] = s;  // inclusive warp prefix
+    }
+    __syncthreads();
+    const int before = (warp > 0 ? wsum[warp - 1] : 0) + x - v;
+    *tot = wsum[nw - 1];
+    return before;
+}
 
 __global__ void k_flag_count(const uint8_t* __restrict__ flags, int64_t n, int64_t* __restrict__ cnt) {
-    __shared__ double red[kBlock];
-    const int64_t c0 = (int64_t)blockIdx.x * kChunkC;
-    double c = 0.0;
-    for (int j = threadIdx.x; j < kChunkC; j += blockDim.x) {
-        const int64_t i = c0 + j;
-        if (i < n) c += flags[i];
-    }
-    const double s = block_sum(c, red);
-    if (threadIdx.x == 0) cnt[blockIdx.x] = (int64_t)s;
+    __shared__ int wsum[32];
+    const bool vec = ((uintptr_t)flags & 15) == 0;
+    uint32_t w[4];
+    const int c = flags16(flags, (int64_t)blockIdx.x * kChunkC + threadIdx.x * 16, n, vec, w);
+    int tot;
+    block_excl_scan(c, wsum, &tot);
+    if (threadIdx.x == 0) cnt[blockIdx.x] = tot;
 }
 
 __global__ void k_scan_counts(int64_t* cnt, int64_t nc, int64_t* total) {
-    // single block, exclusive scan in place (sequential per thread segment)
-    __shared__ int64_t seg[1024];
-    const int t = threadIdx.x;
+    // single block: each thread a contiguous segment, block-wide shuffle scan of the segment sums
+    __shared__ long long wsum[32];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
     const int64_t per = (nc + blockDim.x - 1) / blockDim.x;
     const int64_t b = t * per, e = min(nc, b + per);
-    int64_t s = 0;
+    long long s = 0;
     for (int64_t i = b; i < e; ++i) s += cnt[i];
-    seg[t] = s;
+    long long x = s;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
     __syncthreads();
-    if (t == 0) {
-        int64_t a = 0;
-        for (int u = 0; u < (int)blockDim.x; ++u) {
-            const int64_t v = seg[u];
-            seg[u] = a;
-            a += v;
+    if (warp == 0) {
+        long long v = lane < nw ? wsum[lane] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, v, d);
+            if (lane >= d) v += y;
         }
-        *total = a;
+        if (lane < nw) wsum[lane] = v;
     }
     __syncthreads();
-    int64_t a = seg[t];
+    long long a = (warp > 0 ? wsum[warp - 1] : 0) + x - s;
+    if (t == blockDim.x - 1) *total = a + s;
     for (int64_t i = b; i < e; ++i) {
         const int64_t v = cnt[i];
         cnt[i] = a;
@@ -1496,30 +1550,18 @@ __global__ void k_scan_counts(int64_t* cnt, int64_t nc, int64_t* total) {
 
 __global__ void k_write_indices(const uint8_t* __restrict__ flags, int64_t n, const int64_t* __restrict__ offs,
                                 int64_t base, int64_t* __restrict__ out) {
-    __shared__ int cnt[kBlock];
-    constexpr int PER = kChunkC / kBlock;  // 16 consecutive events per thread
-    const int64_t c0 = (int64_t)blockIdx.x * kChunkC + threadIdx.x * PER;
-    int c = 0;
-    for (int j = 0; j < PER; ++j) {
-        const int64_t i = c0 + j;
-        if (i < n) c += flags[i];
-    }
-    cnt[threadIdx.x] = c;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int a = 0;
-        for (int u = 0; u < kBlock; ++u) {
-            const int v = cnt[u];
-            cnt[u] = a;
-            a += v;
-        }
-    }
-    __syncthreads();
-    int64_t o = offs[blockIdx.x] + cnt[threadIdx.x];
-    for (int j = 0; j < PER; ++j) {
-        const int64_t i = c0 + j;
-        if (i < n && flags[i]) out[o++] = base + i;
-    }
+    __shared__ int wsum[32];
+    const bool vec = ((uintptr_t)flags & 15) == 0;
+    const int64_t c0 = (int64_t)blockIdx.x * kChunkC + threadIdx.x * 16;
+    uint32_t w[4];
+    const int c = flags16(flags, c0, n, vec, w);
+    int tot;
+    const int before = block_excl_scan(c, wsum, &tot);
+    if (!c) return;
+    int64_t o = offs[blockIdx.x] + before;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        for (uint32_t x = w[q] & 0x01010101u; x; x &= x - 1) out[o++] = base + c0 + 4 * q + (__ffs(x) - 1) / 8;
 }
 
 void launch_compact(const uint8_t* flags, int64_t n, int64_t index_base, int64_t* counts_scratch, int64_t* out_idx,

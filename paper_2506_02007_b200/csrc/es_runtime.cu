@@ -168,6 +168,10 @@ bool is_device_ptr(const void* p) {
 // ================================================================ structs
 struct es_ctx {
     int device = 0, rank = 0, world = 1;
+    // the parameters last uploaded and derived into `model` (model_for skips the upload, the
+    // Cholesky launch and its status round trip when a call passes the same model again)
+    std::vector<double> mkey;
+    const double* mkey_dev = nullptr;
     int mode = 0;  // 0 single, 1 nccl, 2 host exchange
     ncclComm_t comm = nullptr;
     es_exchange ex{};
@@ -517,6 +521,18 @@ void check_params(const es_gmm_params* p, int D) {
 double* model_for(es_ctx* c, const es_gmm_params* p, int D) {
     check_params(p, D);
     double* m = c->model.as<double>(mstride(p->K, D));
+    const size_t K = (size_t)p->K;
+    std::vector<double> key;
+    key.reserve(2 + K + K * D + K * D * D);
+    key.push_back((double)p->K);
+    key.push_back((double)D);
+    key.insert(key.end(), p->weights, p->weights + K);
+    key.insert(key.end(), p->means, p->means + K * D);
+    key.insert(key.end(), p->covariances, p->covariances + K * D * D);
+    if (c->mkey_dev == m && key.size() == c->mkey.size() &&
+        std::memcmp(key.data(), c->mkey.data(), key.size() * sizeof(double)) == 0)
+        return m;  // derived model, centre and scale on the device are those of these parameters
+    c->mkey_dev = nullptr;
     upload_model(c, m, p->K, D, p->weights, p->means, p->covariances);
     // FP64 centre for the mixed-precision scorer: the model's mean sum_k pi_k mu_k
     std::vector<double> cen(D, 0.0);
@@ -535,6 +551,8 @@ double* model_for(es_ctx* c, const es_gmm_params* p, int D) {
                                       8.0 * std::sqrt(std::max(p->covariances[(size_t)k * D * D + j * D + j], 0.0)));
     c->center_host = cen;
     c->center_xs = span > 0.0 && std::isfinite(span) ? std::ldexp(1.0, 4 - (int)std::ceil(std::log2(span))) : 1.0;
+    c->mkey.swap(key);
+    c->mkey_dev = m;
     return m;
 }
 
@@ -573,7 +591,7 @@ void score_launch(es_ctx* c, const double* X, int64_t n, int64_t ld, int D, int 
 size_t score_blocks(es_ctx* c, int D, int K) { return (size_t)2 * std::max(score_grid(D, K, c->num_sms), 2 * c->num_sms) + 2; }
 
 double run_score(es_ctx* c, es_dataset* ds, const double* dmodel, int K, ScoreOut o, const double* center,
-                 const double* center_host, double xs) {
+                 const double* center_host, double xs, bool need_total = true) {
     const int D = ds->D;
     double* bs = c->scratch.as<double>(score_blocks(c, D, K));
     double loc = 0.0;
@@ -583,6 +601,7 @@ double run_score(es_ctx* c, es_dataset* ds, const double* dmodel, int K, ScoreOu
         score_launch(c, ds->X, ds->n_local, ds->ld, D, K, dmodel, center, center_host, xs, o, bs, &nblk,
                      ds->has_xmap ? &ds->xmap : nullptr);
         c->t_end(c->score_ms, c->score_launches);
+        if (!need_total) return 0.0;
         double* red = c->scratch2.as<double>(2);
         launch_reduce_blocks(bs, nblk, 2, red, c->stream, c->ls);
         c->check_launch();
@@ -591,6 +610,7 @@ double run_score(es_ctx* c, es_dataset* ds, const double* dmodel, int K, ScoreOu
         c->sync();
         loc = h[0];
     }
+    if (!need_total) return 0.0;  // every rank (empty shards too): no exchange skipped on one rank only
     std::vector<double> all = c->allgather_host(&loc, 1);
     double tot = 0.0;
     for (double v : all) tot += v;
@@ -2041,7 +2061,7 @@ int es_gmm_detect(es_ctx* c, es_dataset* ds, const es_gmm_params* p, double log_
         o.log_delta = log_delta;
         o.mode = mode;
         o.sum_ll = 0;  // detect reports no log-likelihood
-        run_score(c, ds, m, p->K, o, c->center.as<double>(ds->D), c->center_host.data(), c->center_xs);
+        run_score(c, ds, m, p->K, o, c->center.as<double>(ds->D), c->center_host.data(), c->center_xs, false);
         int64_t* cnt = c->scratch2.as<int64_t>((n + 4095) / 4096 + 2);
         int64_t* dcount = cnt + (n + 4095) / 4096 + 1;
         launch_compact(dflags, n, ds->row_offset, cnt, o_idx.dev, dcount, c->stream, c->ls);
@@ -2052,9 +2072,10 @@ int es_gmm_detect(es_ctx* c, es_dataset* ds, const es_gmm_params* p, double log_
         o_bk.finish(c->stream);
         o_bl.finish(c->stream);
         c->sync();
-        if (o_idx.user && o_idx.dev != o_idx.user && local)
+        if (o_idx.user && o_idx.dev != o_idx.user && local) {
             CU(cudaMemcpyAsync(o_idx.user, o_idx.dev, local * 8, cudaMemcpyDeviceToHost, c->stream));
-        c->sync();
+            c->sync();
+        }
         if (n == 0) local = 0;
         if (n_local_flagged) *n_local_flagged = local;
         long long g = local;

@@ -75,10 +75,16 @@ def test_two_ranks_match_single_rank(tmp_path):
     assert np.allclose(z0["per"], m.fit_report.per_iteration_log_likelihoods, rtol=1e-7)
     d, ld = es.calibrate_threshold(m, ds, 0.01, n_train=n // 2, return_log=True)
     assert abs(ld - float(z0["ld"])) <= 1e-6 * abs(ld)
-    r = es.detect(m, ds, log_delta=float(z0["ld"]))
     both = np.concatenate([z0["idx"], z1["idx"]])
     assert int(z0["nflag"]) == int(z1["nflag"]) == len(both)
-    assert len(np.setxor1d(both, r.anomaly_indices)) <= 1e-4 * n  # models differ at 1e-8: threshold band only
+    # the ranks' own model and threshold on the single-rank context: the same flags, except
+    # events within 1e-9 of the threshold (counted from the best-component densities)
+    mr = es.GmmModel(z0["w"], z0["mu"], z0["cov"])
+    bl = np.empty(n)
+    r = es.detect(mr, ds, log_delta=float(z0["ld"]), best_logdens=bl)
+    band = np.abs(bl - float(z0["ld"])) <= 1e-9 * max(1.0, abs(float(z0["ld"])))
+    diff = np.setxor1d(both, r.anomaly_indices)
+    assert np.all(band[diff]), (len(diff), int(band.sum()))
     mk = es.fit_em(ds, 4, init="kmeans++", tol=0.0, max_iter=3, seed=5)
     assert np.allclose(z0["kmu"], mk.means, rtol=1e-5, atol=1e-6)
     # k-means baseline: rank-ordered Lloyd sums -> the same centroids / threshold on both ranks
