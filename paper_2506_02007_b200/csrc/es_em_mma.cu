@@ -159,6 +159,11 @@ __global__ void __launch_bounds__(nthr(NWG), 1) k_em_mma(const __grid_constant__
     if (warp < 4) {  // ones in K columns 0-2 of every row: the bias dispatch's A operand
         const uint32_t one[8] = {0x3C003C00u, 0x00003C00u, 0u, 0u, 0u, 0u, 0u, 0u};  // K columns 0, 1, 2
         tmem_st8(tmem + ((uint32_t)(32 * warp) << 16) + TONE, one);
+        if (NPASS == 2) {  // the s_l columns start at zero (only the R_h^T pass writes them, accumulating)
+            const uint32_t zero[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+            for (int rg = 0; rg < 2; ++rg)
+                tmem_st8(tmem + ((uint32_t)(32 * warp) << 16) + MREG0 + MREGS * rg + TM + KMAX, zero);
+        }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
     tc_fence_before();
@@ -213,6 +218,11 @@ __global__ void __launch_bounds__(nthr(NWG), 1) k_em_mma(const __grid_constant__
                 tmem_ld2(tmem + lq + xg + TM + KMAX + 2 * q, e0, e1);
                 tmem_wait_ld();
                 m1 = hsel ? f1 + e1 : f0 + e0;
+                // zero the s_l columns for the region's next Gram (its first dispatches are the lo
+                // passes, which do not write them)
+                const uint32_t zero[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+                tmem_st8(tmem + lq + xg + TM + KMAX, zero);
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             } else {
                 tmem_wait_ld();
                 m1 = hsel ? f1 : f0;
@@ -562,15 +572,19 @@ __global__ void __launch_bounds__(nthr(NWG), 1) k_em_mma(const __grid_constant__
                 const uint32_t xg = tmem + (uint32_t)(MREG0 + MREGS * (int)(jm & 1));
                 const uint64_t dh = mw == 0 ? dh0[0] : (mw == 1 ? dh0[1] : dh0[NWG - 1]);
                 const uint64_t dl = mw == 0 ? dl0[0] : (mw == 1 ? dl0[1] : dl0[NWG - 1]);
-#pragma unroll
-                for (int ks = 0; ks < TM / 16; ++ks) mma_f16(xg, dh + 16 * ks, dh + 16 * ks, idesc1, ks > 0 ? 1u : 0u);
                 if (NPASS == 2) {
+                    // the small lo products first: the FP32 accumulator truncates ~1 ulp of its running
+                    // sum per dispatch, so lo dispatches issued after the big R_h^T R_h ones tripled
+                    // the Gram's same-sign truncation bias (the s_l columns were zeroed by the flush)
 #pragma unroll
                     for (int ks = 0; ks < TM / 16; ++ks) {
-                        mma_f16(xg, dl + 16 * ks, dh + 16 * ks, idesc2a, 1u);
-                        mma_f16(xg + TM, dl + 16 * ks, dh + (18 * GRP >> 4) + 16 * ks, idesc2b, 1u);
+                        mma_f16(xg, dl + 16 * ks, dh + 16 * ks, idesc2a, ks > 0 ? 1u : 0u);
+                        mma_f16(xg + TM, dl + 16 * ks, dh + (18 * GRP >> 4) + 16 * ks, idesc2b, ks > 0 ? 1u : 0u);
                     }
                 }
+#pragma unroll
+                for (int ks = 0; ks < TM / 16; ++ks)
+                    mma_f16(xg, dh + 16 * ks, dh + 16 * ks, idesc1, (NPASS == 2 || ks > 0) ? 1u : 0u);
                 commit(&S.mdone[mw]);
                 TRACE(10, jm);
             }

@@ -613,15 +613,18 @@ __global__ void __launch_bounds__(WNT, 1)
                         for (int ks = 0; ks < TM / 16; ++ks)
                             mma_f16(tmem + TGR, dh + 16 * ks, dh + 16 * ks, idesc_f16(128, 136, 1), ks > 0 ? 1u : 0u);
                     } else {
+                        // the small lo products first: the FP32 accumulator truncates ~1 ulp of its
+                        // running sum per dispatch, so the 16 lo dispatches issued after the 8 big
+                        // R_h^T R_h ones tripled the Gram's same-sign truncation bias
 #pragma unroll
-                        for (int ks = 0; ks < TM / 16; ++ks)  // R_h^T [R_h | s_h | s_l]
-                            mma_f16(tmem + TGR, dh + 16 * ks, dh + 16 * ks, idesc_f16(128, 144, 1), ks > 0 ? 1u : 0u);
-#pragma unroll
-                        for (int ks = 0; ks < TM / 16; ++ks)  // + R_l^T [R_h | s_h]
-                            mma_f16(tmem + TGR, dl + 16 * ks, dh + 16 * ks, idesc_f16(128, 136, 1), 1u);
+                        for (int ks = 0; ks < TM / 16; ++ks)  // R_l^T [R_h | s_h | s_l] (+ the lo*lo term)
+                            mma_f16(tmem + TGR, dl + 16 * ks, dh + 16 * ks, idesc_f16(128, 144, 1), ks > 0 ? 1u : 0u);
 #pragma unroll
                         for (int ks = 0; ks < TM / 16; ++ks)  // + R_h^T R_l
                             mma_f16(tmem + TGR, dh + 16 * ks, dl + 16 * ks, idesc_f16(128, 128, 1), 1u);
+#pragma unroll
+                        for (int ks = 0; ks < TM / 16; ++ks)  // + R_h^T [R_h | s_h | s_l]
+                            mma_f16(tmem + TGR, dh + 16 * ks, dh + 16 * ks, idesc_f16(128, 144, 1), 1u);
                     }
                     commit(&S.mdone);
                 }

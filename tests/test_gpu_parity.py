@@ -364,14 +364,16 @@ def test_detect_properties_full_size(es):
         prev = f
 
 
-@pytest.mark.parametrize("mode,kernel", [("1", "k_em_diag_tc"), ("0", "k_em_diag_mixed")])
-def test_diag_mixed_pass_parity(es, oracle, mode, kernel, monkeypatch):
+@pytest.mark.parametrize("mode,kernel,n", [("1", "k_em_diag_tc", 1 << 23), ("0", "k_em_diag_mixed", 1 << 23),
+                                           ("1", "k_em_diag_tc", (1 << 24) + 77)])
+def test_diag_mixed_pass_parity(es, oracle, mode, kernel, n, monkeypatch):
     """Diagonal covariances, every component >= 2^20 events: the default tcgen05 pass
     (k_em_diag_tc, E-step quadratic form and M-step moments on the tensor cores) and the FP32
     SIMT pass (k_em_diag_mixed, ES_EM_DIAG_TC=0) against the oracle (c3's kernels at a
-    parity-testable size)."""
+    parity-testable size; 2^24 + 77 events: a ragged last tile and every component >= 2^20
+    events from the first iteration on)."""
     monkeypatch.setenv("ES_EM_DIAG_TC", mode)
-    n, D, K, iters = 1 << 23, 16, 4, 8
+    D, K, iters = 16, 4, 8
     ds, X = syn(es, oracle, n, D, K, seed=3)
     em = es.EM(ds, K, init="random", tol=0.0, max_iter=iters, seed=5, covariance_type="diag")
     em.step(iters)
@@ -428,13 +430,16 @@ def test_full_mixed_pass_parity(es, oracle, n, D, K, iters, monkeypatch):
         rep["final_log_likelihood"])
 
 
-@pytest.mark.parametrize("n,D,K,iters", [(1 << 22, 32, 32, 4), (1 << 22, 24, 12, 4), (1 << 24, 32, 4, 4)])
+@pytest.mark.parametrize("n,D,K,iters", [(1 << 22, 32, 32, 4), (1 << 22, 24, 12, 4), (1 << 24, 32, 4, 4),
+                                         ((1 << 22) + 45, 20, 6, 3)])
 def test_wide_pass_parity(es, oracle, n, D, K, iters):
     """The default full-covariance pass beyond k_em_mma's shapes (D, K <= 32; BASELINE c5 is
     D = K = 32): k_em_wide, E-step whitening and M-step Gram on tcgen05, against the oracle.
     hi + lo records in the first iteration and while some component holds < 2^20 events; the
     D = 32, K = 4 case reaches one-fp16 records (SYN-v1 weights are (k + 1) / 10, so the
-    smallest component holds ~1.7e6 > 2^20 events at N = 2^24)."""
+    smallest component holds ~1.7e6 > 2^20 events at N = 2^24).  2^22 + 45 events: a ragged
+    last tile (and an early trajectory that amplified the pass's Gram bias before the lo
+    products were issued first: weights margin 1.006 -> 0.33)."""
     ds, X = syn(es, oracle, n, D, K, seed=13)
     em = es.EM(ds, K, init="random", tol=0.0, max_iter=iters, seed=2)
     kern = []
