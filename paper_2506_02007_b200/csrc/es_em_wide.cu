@@ -54,7 +54,9 @@ constexpr int KSMAX = (WD + FKS - 1) / FKS;  // 3
 constexpr uint32_t WIMG = 2 * KSMAX * WOP; // group image: (hi, lo) per K-step
 constexpr uint32_t RG = (TM / 8) * 128;    // 2048 B: one MN-major 8-column group of records
 constexpr int RHG = 18, RLG = 16;          // record groups: R_h (16) | s_h | s_l, then R_l (NPASS = 2)
-constexpr uint32_t RECB = (RHG + RLG) * RG;
+// NPASS = 1: two R_h buffers (the records of group m are written while the Gram of group m - 1
+// runs); NPASS = 2: one R_h + R_l buffer
+constexpr uint32_t RECB = (2 * RHG > RHG + RLG ? 2 * RHG : RHG + RLG) * RG;
 constexpr int NSLOT = 3;                   // group-image ring slots
 constexpr int WNT = 128 + 64;              // epilogue WG, TMA warp, MMA warp
 constexpr int TE = 0, TGR = 256, TAX = 400;  // TMEM columns: E x 2, Gram (144), A (hi, lo) x KSMAX
@@ -487,12 +489,15 @@ __global__ void __launch_bounds__(WNT, 1)
                 __syncwarp();
                 if (lane == 0) arrive(&S.gfree);
             };
-            unsigned char* rp = S.rec + (p >> 3) * 128 + (p & 7) * 16;  // R_h groups, then R_l at RHG
+            unsigned char* const rp0 = S.rec + (p >> 3) * 128 + (p & 7) * 16;  // R_h groups, then R_l at RHG
 #pragma unroll
             for (int g = 0; g < WK / CG; ++g) {
                 if (g >= NG) break;
                 const int64_t m = jj * NG + g;
-                if (g >= 1) flush(m - 1);  // the records buffer is free once Gram m - 1 completed
+                // NPASS = 2: one records buffer, free once Gram m - 1 completed; NPASS = 1: buffer
+                // m & 1 (Gram m - 2 was flushed in the previous group), Gram m - 1 flushed after
+                if (NPASS == 2 && g >= 1) flush(m - 1);
+                unsigned char* const rp = rp0 + (NPASS == 1 ? (uint32_t)(m & 1) * RHG * RG : 0u);
 #pragma unroll
                 for (int kl = 0; kl < CG; ++kl) {
                     const float sk = w[CG * g + kl];
@@ -535,6 +540,7 @@ __global__ void __launch_bounds__(WNT, 1)
                     }
                 }
                 proxy_fence();
+                if (NPASS == 1 && g >= 1) flush(m - 1);
                 __syncwarp();
                 if (lane == 0) arrive(&S.mready);
             }
@@ -609,9 +615,10 @@ __global__ void __launch_bounds__(WNT, 1)
                     if (m >= 1) mbar_wait_sleep(su32(&S.gfree), (uint32_t)((m - 1) & 1));
                     tc_fence_after();
                     if (NPASS == 1) {
+                        const uint64_t dhm = sdesc(su32(S.rec) + (uint32_t)(m & 1) * RHG * RG, 128, RG);
 #pragma unroll
                         for (int ks = 0; ks < TM / 16; ++ks)
-                            mma_f16(tmem + TGR, dh + 16 * ks, dh + 16 * ks, idesc_f16(128, 136, 1), ks > 0 ? 1u : 0u);
+                            mma_f16(tmem + TGR, dhm + 16 * ks, dhm + 16 * ks, idesc_f16(128, 136, 1), ks > 0 ? 1u : 0u);
                     } else {
                         // the small lo products first: the FP32 accumulator truncates ~1 ulp of its
                         // running sum per dispatch, so the 16 lo dispatches issued after the 8 big
