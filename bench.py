@@ -73,7 +73,14 @@ class Clocks:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == 6:
-                self.rows.append(parts)
+                self.rows.append((time.perf_counter(), parts))
+
+    def wait_first(self, timeout=5.0):
+        """Block until the sampler delivered a row (nvidia-smi takes ~0.1-1 s to start), so the
+        short timed regions that follow are sampled."""
+        t0 = time.perf_counter()
+        while self.proc and not self.rows and time.perf_counter() - t0 < timeout:
+            time.sleep(0.01)
 
     def __exit__(self, *a):
         if self.proc:
@@ -83,15 +90,22 @@ class Clocks:
             except Exception:
                 self.proc.kill()
 
-    def summary(self):
-        if not self.rows:
+    def summary(self, windows=None):
+        """Clocks and throttle reasons over the samples inside the timed windows [(t0, t1), ...]
+        (every sample when none falls inside; nvidia-smi samples every 20 ms)."""
+        rows = self.rows
+        if windows:
+            inside = [r for r in rows if any(a <= r[0] <= b for a, b in windows)]
+            rows = inside or rows
+        rows = [r[1] for r in rows]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows)}
 
 
 def dist_setup(n_gpus):
@@ -221,6 +235,10 @@ def run_ours(args):
     # ------------------------------------------------------------ EM steps
     total = args.warmup + args.steps
     em = es.EM(ds, K, init="random", tol=0.0, max_iter=total + 1, seed=7)
+    # nvidia-smi sampler over the whole run, summarised over the timed windows only
+    clk = Clocks(local).__enter__()
+    clk.wait_first()
+    windows = []
     # timing mode on for the warm-up too: the iteration graphs with the timing events are
     # captured there, not inside the timed region
     lib.es_ctx_set_timing(ctx.handle, 1)
@@ -231,11 +249,12 @@ def run_ours(args):
     l0 = ctx.launch_count
     c0 = ctx.collective_count
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
-        e0.record(stream)
-        em.step(args.steps)
-        e1.record(stream)
-        torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    e0.record(stream)
+    em.step(args.steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    windows.append((w0, time.perf_counter()))
     em_launches = ctx.launch_count - l0
     em_collectives = ctx.collective_count - c0
     em_ms = e0.elapsed_time(e1)
@@ -264,6 +283,7 @@ def run_ours(args):
     sk_ms0, sk_n0 = ktime(1)
     l1 = ctx.launch_count
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
     s0.record(stream)
     nflag = 0
     for _ in range(args.steps):
@@ -271,6 +291,8 @@ def run_ours(args):
         nflag = r.n_flagged
     s1.record(stream)
     torch.cuda.synchronize()
+    windows.append((w0, time.perf_counter()))
+    clk.__exit__(None, None, None)
     sc_launches = ctx.launch_count - l1
     sc_ms = max_over_ranks(s0.elapsed_time(s1), world)
     sk_ms, sk_n = ktime(1)
@@ -344,7 +366,7 @@ def run_ours(args):
         "gpu_launches": em_launches,
         "nccl_collectives": em_collectives,
         "gpu_launches_score": sc_launches,
-        "clocks": clk.summary(),
+        "clocks": clk.summary(windows),
         "e2e": e2e,
     }
     if not args.no_cpu_baseline and world == 1:
