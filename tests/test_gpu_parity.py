@@ -364,16 +364,18 @@ def test_detect_properties_full_size(es):
         prev = f
 
 
-@pytest.mark.parametrize("mode,kernel,n", [("1", "k_em_diag_tc", 1 << 23), ("0", "k_em_diag_mixed", 1 << 23),
-                                           ("1", "k_em_diag_tc", (1 << 24) + 77)])
-def test_diag_mixed_pass_parity(es, oracle, mode, kernel, n, monkeypatch):
+@pytest.mark.parametrize("mode,kernel,n,D,K", [("1", "k_em_diag_tc", 1 << 23, 16, 4),
+                                               ("0", "k_em_diag_mixed", 1 << 23, 16, 4),
+                                               ("1", "k_em_diag_tc", (1 << 24) + 77, 16, 4),
+                                               ("1", "k_em_diag_tc", 1 << 24, 10, 5)])
+def test_diag_mixed_pass_parity(es, oracle, mode, kernel, n, D, K, monkeypatch):
     """Diagonal covariances, every component >= 2^20 events: the default tcgen05 pass
     (k_em_diag_tc, E-step quadratic form and M-step moments on the tensor cores) and the FP32
     SIMT pass (k_em_diag_mixed, ES_EM_DIAG_TC=0) against the oracle (c3's kernels at a
     parity-testable size; 2^24 + 77 events: a ragged last tile and every component >= 2^20
-    events from the first iteration on)."""
+    events from the first iteration on; D = 10, K = 5: padded features and components)."""
     monkeypatch.setenv("ES_EM_DIAG_TC", mode)
-    D, K, iters = 16, 4, 8
+    iters = 8
     ds, X = syn(es, oracle, n, D, K, seed=3)
     em = es.EM(ds, K, init="random", tol=0.0, max_iter=iters, seed=5, covariance_type="diag")
     em.step(iters)
