@@ -325,7 +325,11 @@ __global__ void __launch_bounds__(NTHR, 1) k_score_mma(const __grid_constant__ C
 #ifdef ES_SCORE_COUNT
             if (valid) atomicAdd(&g_score_pairs, (unsigned long long)(1 + __popc(extra)));
 #endif
+#ifdef ES_SCORE_KB0  // diagnostic (wrong answers): every lane recomputes component 0, i.e. W loads all broadcast
+            const double lp = (valid && refine_all != 3) ? refine(s, p, 0) : (double)ln[kb];
+#else
             const double lp = (valid && refine_all != 3) ? refine(s, p, kb) : (double)ln[kb];
+#endif
             // extra pairs: compacted per warp (lane order, then component), one pair per lane
             double* lnv = S.lnv[w];
             const unsigned any = __ballot_sync(0xffffffffu, extra != 0);
