@@ -89,7 +89,8 @@ struct SmemDT {
 constexpr int ECOL = 0;                          // E accumulator of WG w: columns 32 w (hi Theta_hi + lo Theta_hi | hi Theta_lo)
 constexpr int MCOL = 32 * NWG_DTC;               // M accumulators of WG w: MCOL + 32 NACC w
 static_assert(sizeof(((SmemDT*)0)->grec) >= 4 * SGB, "junk rows of the last record");
-static_assert(MCOL + 32 * NACC * NWG_DTC <= 256, "TMEM columns");
+constexpr uint32_t TCOLS = MCOL + 32 * NACC * NWG_DTC <= 256 ? 256 : 512;  // TMEM allocation (power of two)
+static_assert(MCOL + 32 * NACC * NWG_DTC <= 512, "TMEM columns");
 
 }  // namespace
 
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(nthr_dtc(), 1)
         *reinterpret_cast<__half*>(S.bt[g] + kmaj(KC + k, s)) = hl;
     }
     if (warp == WE) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(&S.tmem)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&S.tmem)), "r"(TCOLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (t == 0) {
@@ -439,7 +440,7 @@ __global__ void __launch_bounds__(nthr_dtc(), 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (warp == WE) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    if (warp == WE) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
 }
 
 // ES_EM_DIAG_TC=0 keeps the FP32 SIMT k_em_diag_mixed pass; =2 (diagnostics) also takes
