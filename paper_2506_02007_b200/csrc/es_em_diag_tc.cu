@@ -26,7 +26,8 @@
 // running sum of the FP32 accumulator (truncated ~1 ulp per dispatch, scripts/umma_probe.cu) is
 // a partial log density (of the size of w) rather than of the size of the separate terms.
 // M-step per 16-event K-step: records^T [2^10 gamma hi | lo] (M128 N32 K16), rows = statistics, into
-// NACC TMEM accumulators used round robin (fewer same-sign truncations per accumulator), read by
+// NACC = 2 TMEM accumulators used round robin (fewer same-sign truncations per accumulator: at the
+// c3 config itself the covariance margin is 0.23 with two, 0.86 with one, for ~13% of pass time), read by
 // thread = statistic row after every tile and accumulated in compensated FP32 pairs; the hi and lo
 // rows of x^2 and x^ and the '1' row give the moments to ~2^-22 per event (a single fp16 rounding
 // of x^2 left a 2^-12 / sqrt(N_k) noise that dominated the covariance error); gamma is split
@@ -43,7 +44,7 @@
 #include "es_mma.cuh"
 
 #ifndef ES_DTC_NACC
-#define ES_DTC_NACC 1
+#define ES_DTC_NACC 2
 #endif
 #ifndef ES_DTC_NWG  // epilogue warpgroups
 #define ES_DTC_NWG 3
