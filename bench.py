@@ -135,13 +135,13 @@ def max_over_ranks(v, world):
     return float(t.item())
 
 
-def cpu_em_setup(cores, X=None):
+def cpu_em_setup(cores, X=None, n=N_GLOBAL):
     """The bench workload on the host for the CPU oracle: the full N=2^26 SYN-v1 matrix (the
     same rows the device generator writes) and the same Random init (seed 7)."""
     from oracle import oracle
     if X is None:
         model = oracle.syn_model(SEED, D, K)
-        X, _, _ = oracle.syn_rows(SEED, D, K, model, 0, N_GLOBAL, nthreads=cores)
+        X, _, _ = oracle.syn_rows(SEED, D, K, model, 0, n, nthreads=cores)
     pi, mu, cov, reg = oracle.random_init(X, K, 7)
     return X, pi, mu, cov, reg
 
@@ -170,8 +170,9 @@ def run_reference(args):
         return
     from oracle import oracle
     cores = os.cpu_count()
+    n_global = args.n or N_GLOBAL  # --n: debug / CPU-test size only
     t0 = time.perf_counter()
-    X, pi, mu, cov, reg = cpu_em_setup(cores)
+    X, pi, mu, cov, reg = cpu_em_setup(cores, n=n_global)
     setup_s = time.perf_counter() - t0
     for _ in range(args.warmup):
         oracle.em_step(X, pi, mu, cov, reg, nthreads=cores)
@@ -185,11 +186,11 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (SYN-v1 seed 42, generated on the host by the oracle)",
-            "config": {"workload": WORKLOAD, "N": N_GLOBAL, "D": D, "K": K, "covariance": "full",
+            "config": {"workload": WORKLOAD, "N": n_global, "D": D, "K": K, "covariance": "full",
                        "init": "random seed 7"},
             "cpu_baseline": {"value": v, "unit": "iters/s", "cores": cores, "kind": "port",
                              "sample": f"every step: 1 EM iteration (oracle eso_em_step: E-step + two-pass "
-                                       f"M-step) on the full {N_GLOBAL}x{D} matrix, {cores} OpenMP threads, "
+                                       f"M-step) on the full {n_global}x{D} matrix, {cores} OpenMP threads, "
                                        f"after {args.warmup} untimed warm-up iterations; host generation + "
                                        f"init {setup_s:.1f} s untimed"},
             "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
