@@ -901,7 +901,10 @@ int em_choose_path(const es_em_state* st) {
     if (em_wide_mode() == 3 && c->precision == 0 && em_wide_supported(st->D, st->K) && st->min_nk >= kMixedMinNk)
         return wide_path(st);
     if (mixed_em(c, st) && em_mma_enabled() && ds->has_xmap) {
-        const int np = em_mma_passes() ? em_mma_passes() : (st->min_nk >= kOnePassMinNk ? 1 : 2);
+        // one fp16 record per value once every component held >= 2^20 events in the previous
+        // M-step; hi + lo records otherwise and in the first iteration (the initial weights are
+        // not event counts: the bench trajectory's first E-step leaves a component 225k events)
+        const int np = em_mma_passes() ? em_mma_passes() : ((st->t > 0 && st->min_nk >= kOnePassMinNk) ? 1 : 2);
         return np == 1 ? kPathMma1 : kPathMma2;
     }
     if (mixed_full(c, st)) {
