@@ -170,7 +170,7 @@ def run_reference(args):
         return
     from oracle import oracle
     cores = os.cpu_count()
-    n_global = args.n or N_GLOBAL  # --n: debug / CPU-test size only
+    n_global = args.rows or N_GLOBAL  # --rows: debug / CPU-test size only
     t0 = time.perf_counter()
     X, pi, mu, cov, reg = cpu_em_setup(cores, n=n_global)
     setup_s = time.perf_counter() - t0
@@ -222,7 +222,7 @@ def run_ours(args):
         exchange = "host gloo (ranks share a GPU: functional check, not a scaling number)"
     else:
         ctx = es.Context(local)
-    n_global = args.n or N_GLOBAL
+    n_global = args.rows or N_GLOBAL
     ds = es.Dataset.generate(SEED, n_global, D, K, ctx=ctx)
     stream = torch.cuda.ExternalStream(ctx.stream)
     lib = ctx._lib
@@ -393,7 +393,9 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=0, help="override N (debug only)")
+    # (not "--n": torchrun, which re-runs this script for --gpus N, would take it as an ambiguous
+    # prefix of its own --nnodes / --nproc-per-node options)
+    ap.add_argument("--rows", type=int, default=0, help="override N (debug and CPU tests only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--traffic", type=float, default=8590144000.0 + 4064256.0,

@@ -61,3 +61,19 @@ def test_model_cache_tracks_parameter_changes(es):
     es.score(m, ds, ll=ll4)
     r4 = es.detect(m, ds, log_delta=ld)
     assert np.array_equal(ll4, ll1) and np.array_equal(r4.anomaly_indices, r1.anomaly_indices)
+
+
+def test_bench_two_ranks_functional():
+    """`bench.py --gpus 2` without a launcher re-runs itself as two ranks (torch.distributed.run on
+    127.0.0.1); on a one-GPU box both ranks share it through the host exchange (a functional
+    check of the multi-rank bench path, not a scaling number).  Rank 0 prints one JSON line."""
+    import json
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "2", "--warmup",
+                          "3", "--rows", str(1 << 20), "--no-e2e", "--no-cpu-baseline"], capture_output=True, text=True,
+                         timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["steps"] == 2 and d["warmup"] == 3
+    assert d["config"]["N"] == 1 << 20 and "exchange" in d["config"]
