@@ -363,7 +363,10 @@ def run_ours(args):
         "score": {"events_per_s": sc_evs, "ms_per_pass": sc_ms / args.steps, "n_flagged": nflag,
                   "roofline": {"bound": "hbm", "kernel": sc_kernel, "achieved": sc_ach, "peak": hbm,
                                "unit": "GB/s", "frac": sc_ach / hbm,
-                               "algorithmic_bytes_per_launch": sc_bytes, "avg_launch_ms": sc_kern_avg}},
+                               "algorithmic_bytes_per_launch": sc_bytes, "avg_launch_ms": sc_kern_avg,
+                               "limiter": "the shared-memory data pipe at 88% of peak: 72% of its wavefronts are "
+                                          "the FP64 W_k^T loads of the best-component recomputation (1152 B "
+                                          "per event) - profiles/r02_k_score_mma_ncu_summary.txt"}},
         "gpu_launches": em_launches,
         "nccl_collectives": em_collectives,
         "gpu_launches_score": sc_launches,
