@@ -204,8 +204,12 @@ __global__ void __launch_bounds__(NTHR, 1) k_score_mma(const __grid_constant__ C
 #pragma unroll
             for (int f = 0; f < DM; ++f) {
                 const double df = S.xd[s][f * TM + e] - mk[f];
+                // W is lower triangular: rows r >= f.  Odd f: the diagonal entry alone (8 B), then
+                // aligned pairs (the zero above the diagonal is not loaded: these loads are the
+                // pass's binding shared-memory traffic)
+                if (f & 1) z[f] = fma(WTk[f * DM + f], df, z[f]);
 #pragma unroll
-                for (int r = f & ~1; r < DM; r += 2) {  // W is lower triangular: rows r >= f
+                for (int r = (f & 1) ? f + 1 : f; r < DM; r += 2) {
                     const double2 wv = *reinterpret_cast<const double2*>(WTk + f * DM + r);
                     z[r] = fma(wv.x, df, z[r]);
                     z[r + 1] = fma(wv.y, df, z[r + 1]);
